@@ -1,0 +1,276 @@
+"""Oracle pin: re-expresses proj/tests/test_drivers.cpp, test_matmodel.cpp and
+acceptance C4/C5/C7/C8/C9/C10 (proj/tests/acceptance.cpp) against the oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+I11 = O.SearchInterval(-1, 1)
+
+
+def small_instance(seed, n=24, inside=5):  # test_drivers.cpp:14-18
+    lay = O.SpectrumLayout(n, O.SearchInterval(-0.9, 0.9), inside, O.SearchInterval(1.6, 12.0),
+                           n - inside, "uniform", 1, 0.0, seed)
+    return O.assemble_matrix(*O.generate_spectrum(lay))
+
+
+def test_matmodel_validation_and_determinism():  # test_matmodel.cpp:26-63
+    with pytest.raises(O.InvalidArgument):
+        O.generate_spectrum(O.SpectrumLayout(10, I11, 5, O.SearchInterval(0.5, 3), 5, seed=1))
+    with pytest.raises(O.InvalidArgument):
+        O.generate_spectrum(O.SpectrumLayout(10, I11, 5, O.SearchInterval(2, 3), 6, seed=1))
+    v, Q = O.generate_spectrum(O.SpectrumLayout(2, I11, 2, O.SearchInterval(2, 3), 0, seed=7))
+    assert list(v) == [-1.0, 1.0]
+    lay = O.SpectrumLayout(24, I11, 6, O.SearchInterval(1.5, 9), 18, seed=123)
+    a, Qa = O.generate_spectrum(lay)
+    b, Qb = O.generate_spectrum(lay)
+    assert np.array_equal(a, b) and np.array_equal(Qa, Qb)
+    assert np.abs(Qa.T @ Qa - np.eye(24)).max() <= 1e-12
+    assert np.all(np.diff(a) >= 0)
+    lay.seed = 124
+    assert not np.array_equal(O.generate_spectrum(lay)[1], Qa)
+    # column sign normalisation: largest-magnitude entry positive
+    idx = np.argmax(np.abs(Qa), axis=0)
+    assert np.all(Qa[idx, np.arange(24)] > 0)
+
+
+def test_assemble_matches_dense_eig():  # test_matmodel.cpp:65-107
+    A = O.assemble_matrix([2.0, 5.0], np.eye(2))
+    assert A[0, 0] == 2.0 and A[1, 1] == 5.0 and A[0, 1] == 0.0
+    lay = O.SpectrumLayout(64, O.SearchInterval(-3, -1), 20, O.SearchInterval(0, 50), 44, seed=7)
+    vals, Q = O.generate_spectrum(lay)
+    w, _ = O.dense_eig(O.assemble_matrix(vals, Q))
+    assert np.abs(w - vals).max() <= 1e-10 * np.abs(vals).max()
+
+
+def test_symmetric_matrix_check():  # matmodel.cpp:10-19
+    M = np.array([[1.0, 2.0], [2.0 + 1e-6, 3.0]])
+    with pytest.raises(O.InvalidArgument):
+        O.symmetric_matrix(M)
+    S = O.symmetric_matrix(np.array([[1.0, 2.0], [2.0 + 1e-13, 3.0]]))
+    assert S[0, 1] == S[1, 0]
+
+
+def test_initial_guess():  # test_drivers.cpp:22-29
+    a = O.make_initial_guess(4, 2, 7)
+    assert np.array_equal(a, O.make_initial_guess(4, 2, 7))
+    assert np.linalg.matrix_rank(O.make_initial_guess(4, 4, 3)) == 4
+    with pytest.raises(O.InvalidArgument):
+        O.make_initial_guess(4, 5, 1)
+
+
+def test_feast_4x4_diagonal():  # test_drivers.cpp:31-44
+    A = np.diag([-0.5, 0.5, 2.0, 3.0])
+    sol = O.feast_solve(A, I11, O.SolverConfig(m0=3, n_c=8, tol=1e-12))
+    assert sol.converged and sol.iterations <= 3
+    assert len(sol.eigenvalues) == 2
+    assert sol.eigenvalues[0] == pytest.approx(-0.5, rel=1e-12)
+    assert sol.eigenvalues[1] == pytest.approx(0.5, rel=1e-12)
+    assert sol.residual_norms.max() <= 1e-12
+
+
+def test_xfeast_2x2():  # test_drivers.cpp:46-56
+    sol = O.xfeast_solve(np.diag([0.5, 2.0]), I11, O.SolverConfig(m0=1, s=2, n_c=8))
+    assert sol.converged and len(sol.eigenvalues) == 1
+    assert sol.eigenvalues[0] == pytest.approx(0.5, rel=1e-12)
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+@pytest.mark.parametrize("driver", ["feast_solve", "xfeast_solve", "rfeast_solve"])
+def test_drivers_vs_dense_oracle(seed, driver):  # test_drivers.cpp:58-95
+    A = small_instance(seed)
+    w, V = O.dense_eig(A)
+    m_true = sum(1 for x in w if I11.contains(x))
+    sol = getattr(O, driver)(A, I11, O.SolverConfig(m0=8, n_c=8, s=2, tol=1e-10))
+    assert sol.converged and len(sol.eigenvalues) == m_true
+    scale = np.linalg.norm(A)
+    for k, lam in enumerate(sol.eigenvalues):
+        j = int(np.argmin(np.abs(w - lam)))
+        assert abs(w[j] - lam) <= 1e-8 * scale
+        assert abs(V[:, j] @ sol.eigenvectors[:, k]) >= 1 - 1e-8
+
+
+def test_empty_interval():  # test_drivers.cpp:97-108
+    sol = O.feast_solve(np.diag([2.0, 3.0, 4.0, 5.0]), I11, O.SolverConfig(m0=2, n_c=4))
+    assert sol.converged and sol.iterations == 1 and len(sol.eigenvalues) == 0
+    assert len(sol.trace) == 1 and sol.trace[0].m_found == 0
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_s1_traces_match_feast(seed):  # test_drivers.cpp:110-135
+    A = small_instance(seed)
+    cfg = O.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=12)
+    f = O.feast_solve(A, I11, cfg)
+    x = O.xfeast_solve(A, I11, cfg)
+    r = O.rfeast_solve(A, I11, cfg)
+    assert len(x.trace) == len(f.trace) == len(r.trace)
+    for tf, tx, tr in zip(f.trace, x.trace, r.trace):
+        tol = 1e-6 * tf.max_residual + 1e-12
+        assert abs(tx.max_residual - tf.max_residual) <= tol
+        assert abs(tr.max_residual - tf.max_residual) <= tol
+        assert tx.rhs_cumulative == tf.rhs_cumulative == tr.rhs_cumulative
+
+
+def test_rhs_accounting_formula():  # test_drivers.cpp:137-160
+    A = small_instance(31)
+    cfg = O.SolverConfig(m0=7, n_c=5, s=3, tol=1e-13, max_iter=6)
+    for rec in O.feast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 7 * rec.iter
+    for rec in O.xfeast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 7 * (rec.iter + max(cfg.s - 2, 0))
+    for rec in O.rfeast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 7 * rec.iter
+
+
+def test_determinism_and_cache_invariance():  # test_drivers.cpp:162-196
+    A = small_instance(41)
+    cfg = O.SolverConfig(m0=6, n_c=4, s=2, max_iter=8, tol=1e-13)
+    for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+        a, b = d(A, I11, cfg), d(A, I11, cfg)
+        assert np.array_equal(a.eigenvalues, b.eigenvalues)
+        assert np.array_equal(a.eigenvectors, b.eigenvectors)
+        assert [t.max_residual for t in a.trace] == [t.max_residual for t in b.trace]
+    A = small_instance(43)
+    cfg = O.SolverConfig(m0=6, n_c=4, max_iter=6, tol=1e-13)
+    plain = O.feast_solve(A, I11, cfg)
+    cfg.cache_factorizations = True
+    cached = O.feast_solve(A, I11, cfg)
+    assert np.array_equal(plain.eigenvalues, cached.eigenvalues)
+    assert plain.accounting.rhs_solved == cached.accounting.rhs_solved
+    assert cached.accounting.factorizations == 4
+
+
+def test_converged_run_ends_at_trace_minimum():  # test_drivers.cpp:198-208
+    sol = O.feast_solve(small_instance(47), I11, O.SolverConfig(m0=7, n_c=6, tol=1e-11))
+    assert sol.converged
+    assert all(sol.trace[-1].max_residual <= r.max_residual for r in sol.trace)
+
+
+def test_rate_prediction():  # test_drivers.cpp:210-243 and acceptance C8
+    cases = [(32, 6, 2.5, 30.0, 61, 6, 6, 1e-14, 30, 42)]
+    for k in range(5):
+        n, m = 28 + 6 * k, 5 + k % 3
+        cases.append((n, m, 2.0 + 0.3 * k, 25.0, 8000 + k, m, 4, 1e-14, 30, 8100 + k))
+    for n, m, olo, ohi, lseed, m0, nc, tol, mi, xseed in cases:
+        lay = O.SpectrumLayout(n, O.SearchInterval(-0.9, 0.9), m, O.SearchInterval(olo, ohi),
+                               n - m, seed=lseed)
+        vals, Q = O.generate_spectrum(lay)
+        A = O.assemble_matrix(vals, Q)
+        rule = O.build_contour_rule(I11, nc)
+        pred = O.predicted_rate(rule, vals, m0)
+        assert pred <= 0.1
+        sol = O.feast_solve(A, I11, O.SolverConfig(m0=m0, n_c=nc, tol=tol, max_iter=mi, seed=xseed))
+        prod, samples = 1.0, 0
+        for a, b in zip(sol.trace[:-1], sol.trace[1:]):
+            if a.max_residual < 1e-2 and a.max_residual > 1e-12 and b.max_residual > 1e-13:
+                prod *= b.max_residual / a.max_residual
+                samples += 1
+        if samples:
+            meas = prod ** (1.0 / samples)
+            assert pred / 10 <= meas <= 10 * pred
+
+
+def test_trace_csv():  # test_drivers.cpp:245-252
+    assert O.write_trace_csv([O.TraceRecord(1, 8, 40, 0.125, 3)]) == (
+        "iter,subspace_dim,rhs_cumulative,max_residual,m_found\n1,8,40,0.125,3\n")
+
+
+def test_config_validation():  # test_drivers.cpp:254-262
+    A = small_instance(3, 12, 3)
+    with pytest.raises(O.InvalidArgument):
+        O.feast_solve(A, I11, O.SolverConfig(m0=0))
+    with pytest.raises(O.InvalidArgument):
+        O.feast_solve(A, I11, O.SolverConfig(m0=4, tol=0.0))
+
+
+def test_acceptance_c4_all_drivers():  # acceptance.cpp:136-195
+    for k in range(10):
+        dense = k % 2 == 1
+        n = 24 + 8 * (k % 5)
+        m = 4 + k % 3
+        lay = O.SpectrumLayout(n, O.SearchInterval(-0.9, 0.9), m,
+                               O.SearchInterval(1.25, 2.2) if dense else O.SearchInterval(1.8, 16.0),
+                               n - m, seed=5000 + k)
+        vals, Q = O.generate_spectrum(lay)
+        A = O.assemble_matrix(vals, Q)
+        m_true = sum(1 for v in vals if I11.contains(v))
+        scale = np.linalg.norm(A)
+        w, V = O.dense_eig(A)
+        Vin = V[:, [i for i in range(n) if I11.contains(w[i])]]
+        cfg = O.SolverConfig(m0=m + 4, n_c=8, s=3, tol=1e-9, max_iter=50, seed=6000 + k)
+        for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+            sol = d(A, I11, cfg)
+            assert sol.converged
+            assert len(sol.eigenvalues) == m_true
+            for j, lam in enumerate(sol.eigenvalues):
+                assert np.abs(w - lam).min() <= 1e-8 * scale
+                v = sol.eigenvectors[:, j]
+                assert np.linalg.norm(v - Vin @ (Vin.T @ v)) <= 1e-6
+
+
+def _benchmark_family(dense, seed=42):  # acceptance.cpp:45-56
+    lay = O.SpectrumLayout(545, I11, 50, O.SearchInterval(1.01, 1.1) if dense
+                           else O.SearchInterval(1.01, 20.81), 495, seed=seed)
+    return O.assemble_matrix(*O.generate_spectrum(lay))
+
+
+KBENCH = O.SearchInterval(-1.005, 1.005)
+
+
+@pytest.mark.slow
+def test_acceptance_c5_contrast():  # acceptance.cpp:199-244
+    sparse = _benchmark_family(False)
+    sol = O.feast_solve(sparse, KBENCH, O.SolverConfig(m0=75, n_c=3, tol=1e-10, max_iter=20,
+                                                       cache_factorizations=True))
+    assert sol.converged and sol.iterations <= 20
+    dense = _benchmark_family(True)
+    sol = O.feast_solve(dense, KBENCH, O.SolverConfig(m0=51, n_c=8, tol=1e-12, max_iter=10,
+                                                      cache_factorizations=True))
+    assert min(r.max_residual for r in sol.trace) > 1e-4
+    for d in (O.xfeast_solve, O.rfeast_solve):
+        sol = d(dense, KBENCH, O.SolverConfig(m0=51, n_c=8, s=3, tol=1e-6, max_iter=25,
+                                              cache_factorizations=True))
+        assert sol.converged
+
+
+def test_acceptance_c7_clustered():  # acceptance.cpp:295-330
+    lay = O.SpectrumLayout(180, I11, 20, O.SearchInterval(1.05, 5.0), 160, "clustered", 4, 0.02, 77)
+    A = O.assemble_matrix(*O.generate_spectrum(lay))
+    I = O.SearchInterval(-1.005, 1.06)
+    cfg = O.SolverConfig(m0=44, n_c=8, tol=1e-13, max_iter=30, cache_factorizations=True)
+    r_feast = O.feast_solve(A, I, cfg).trace[-1].max_residual
+    cfg.s = 3
+    for d in (O.xfeast_solve, O.rfeast_solve):
+        assert d(A, I, cfg).trace[-1].max_residual <= 1e-4 * r_feast
+
+
+def test_acceptance_c9_s1_equivalence():  # acceptance.cpp:390-425
+    for k in range(5):
+        n = 24 + 4 * k
+        lay = O.SpectrumLayout(n, O.SearchInterval(-0.9, 0.9), 5, O.SearchInterval(1.6, 12.0),
+                               n - 5, seed=9000 + k)
+        A = O.assemble_matrix(*O.generate_spectrum(lay))
+        cfg = O.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=15, seed=9100 + k)
+        f, x, r = (d(A, I11, cfg) for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve))
+        assert len(f.trace) == len(x.trace) == len(r.trace)
+        for a, b, c in zip(f.trace, x.trace, r.trace):
+            tol = 1e-6 * a.max_residual + 1e-12
+            assert abs(b.max_residual - a.max_residual) <= tol
+            assert abs(c.max_residual - a.max_residual) <= tol
+
+
+def test_acceptance_c10_determinism_accounting():  # acceptance.cpp:429-472
+    lay = O.SpectrumLayout(40, O.SearchInterval(-0.9, 0.9), 8, O.SearchInterval(1.4, 9.0), 32,
+                           seed=1234)
+    A = O.assemble_matrix(*O.generate_spectrum(lay))
+    cfg = O.SolverConfig(m0=11, n_c=5, s=3, tol=1e-13, max_iter=10)
+    for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+        a, b = d(A, I11, cfg), d(A, I11, cfg)
+        assert O.write_trace_csv(a.trace) == O.write_trace_csv(b.trace)
+        assert np.array_equal(a.eigenvalues, b.eigenvalues)
+    for rec in O.feast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 11 * rec.iter
+    for rec in O.xfeast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 11 * (rec.iter + 1)
+    for rec in O.rfeast_solve(A, I11, cfg).trace:
+        assert rec.rhs_cumulative == 5 * 11 * rec.iter
