@@ -1,0 +1,24 @@
+// Drop-in for proj/include/feastlab/matmodel.hpp: SymmetricMatrix, the
+// hot-path input container. (The synthetic-spectrum generator of the
+// reference is fixture code outside the filter path: SURVEY.md §8(f)(1).)
+#pragma once
+
+#include "feastlab/contour.hpp"
+#include "feastlab/matrix.hpp"
+
+namespace feastlab {
+
+/// Dense real-symmetric operator, symmetrised exactly as (M + M^T)/2 at
+/// construction (matmodel.cpp:10-19); immutable afterwards.
+class SymmetricMatrix {
+public:
+    explicit SymmetricMatrix(MatrixXd entries, double sym_tol = 1e-12);
+    int dim() const { return mat_.rows(); }
+    const MatrixXd& mat() const { return mat_; }
+    double operator()(int i, int j) const { return mat_(i, j); }
+
+private:
+    MatrixXd mat_;
+};
+
+}  // namespace feastlab

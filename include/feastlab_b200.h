@@ -1,0 +1,190 @@
+/*
+ * feastlab_b200.h — the C ABI of the B200-native FEAST filter hot path.
+ *
+ * The reference (feastlab, /root/reference/proj) has no FFI; its public
+ * interface is C++ over Eigen. This header is the thin C boundary that the
+ * drop-in C++ layer (include/feastlab/ headers, same names and options as
+ * the headers in proj/include/feastlab/) and foreign callers (Python ctypes in
+ * paper_1605_08771_b200/) bind. Every entry point below names the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *   - Column-major fp64, explicit leading dimensions. No complex numbers cross
+ *     the ABI except in the NodeFactorization test hook (interleaved re,im).
+ *   - Every function returns an fl_status; on failure *err (may be NULL) holds
+ *     the payload of the reference exception it stands for.
+ *   - loc = FL_HOST: pointer is host memory; FL_DEVICE: pointer is device
+ *     memory on the context's GPU (cudaMalloc / torch), ordered on the
+ *     context stream.
+ *   - Handles (fl_ctx, fl_matrix, fl_block, fl_filter) are not thread-safe;
+ *     calls on one context are serialised by an internal mutex, so concurrent
+ *     solves (CLI `compare` cells, proj/tools/feastlab_cli.cpp:290-292) must
+ *     use one context each or accept serialisation.
+ *   - Not a CPU fallback: without a CUDA device every compute entry returns
+ *     FL_CUDA.
+ */
+#ifndef FEASTLAB_B200_H
+#define FEASTLAB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the C++ layer maps them back to the reference exception types */
+enum fl_status {
+  FL_OK = 0,
+  FL_INVALID_ARGUMENT = 1, /* std::invalid_argument                                  */
+  FL_RUNTIME_ERROR = 2,    /* std::runtime_error                                     */
+  FL_CHOLESKY = 3,         /* feastlab::CholeskyError (ritz.hpp:27-31): pivot, index */
+  FL_SINGULAR_NODE = 4,    /* runtime_error of filterop.cpp:19-22: index, z          */
+  FL_CUDA = 5,
+  FL_NCCL = 6,
+  FL_OOM = 7
+};
+
+enum fl_loc { FL_HOST = 0, FL_DEVICE = 1 };
+
+typedef struct fl_err {
+  int status;
+  int index;     /* CholeskyError::index / singular node index     */
+  double pivot;  /* CholeskyError::pivot                            */
+  double z_re;   /* singular node shift                             */
+  double z_im;
+  char msg[512]; /* what()                                          */
+} fl_err;
+
+typedef struct fl_ctx fl_ctx;       /* device, stream, NCCL communicator, workspaces */
+typedef struct fl_matrix fl_matrix; /* device-resident SymmetricMatrix               */
+typedef struct fl_block fl_block;   /* device-resident n x p real block (MatrixXd)    */
+typedef struct fl_filter fl_filter; /* FilterApplier state (rule, factor cache)       */
+
+/* ------------------------------------------------------------ context */
+int fl_version(void);
+int fl_device_count(int* count);
+/* one GPU, no collective */
+int fl_ctx_create(int device, fl_ctx** out, fl_err* err);
+/* rank `rank` of `nranks` (one process per GPU); contour nodes are sharded
+   across the ranks and the filter sum is all-reduced over NCCL. `nccl_id` is
+   the 128-byte ncclUniqueId made by fl_nccl_unique_id on rank 0. */
+int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl_ctx** out,
+                       fl_err* err);
+int fl_nccl_unique_id(void* out128, fl_err* err);
+int fl_ctx_destroy(fl_ctx* ctx);
+int fl_ctx_sync(fl_ctx* ctx, fl_err* err);
+void* fl_ctx_stream(fl_ctx* ctx); /* cudaStream_t */
+int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks);
+/* number of kernels this context launched so far (instrumentation) */
+long long fl_ctx_launches(const fl_ctx* ctx);
+
+/* ------------------------------------------------------------ matrix
+   SymmetricMatrix (proj/include/feastlab/matmodel.hpp:12-24): the caller has
+   already symmetrised (fl_symmetric_matrix); the device copy is zero-padded. */
+int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_matrix** out,
+                     fl_err* err);
+int fl_matrix_destroy(fl_matrix* m);
+int fl_matrix_dim(const fl_matrix* m);
+
+/* ------------------------------------------------------------ blocks (Eigen::MatrixXd on device) */
+int fl_block_create(fl_ctx* ctx, int n, int cap_cols, fl_block** out, fl_err* err);
+int fl_block_destroy(fl_block* b);
+int fl_block_cols(const fl_block* b);
+int fl_block_rows(const fl_block* b);
+/* upload p columns (p <= capacity) */
+int fl_block_set(fl_block* b, const double* X, int ldx, int p, int loc, fl_err* err);
+/* download all current columns */
+int fl_block_get(const fl_block* b, double* X, int ldx, int loc, fl_err* err);
+/* dst = src[:, idx[0..k-1]] (select_pairs gather, ritz.cpp:153-164; fill_solution) */
+int fl_block_gather(fl_block* dst, const fl_block* src, const int* idx, int k, fl_err* err);
+/* dst = [dst, src] (hconcat, drivers.cpp:84-94; RFEAST expansion, drivers.cpp:224-230) */
+int fl_block_append(fl_block* dst, const fl_block* src, fl_err* err);
+int fl_block_copy(fl_block* dst, const fl_block* src, fl_err* err);
+
+/* ------------------------------------------------------------ filter (THE hot path)
+   FilterApplier(A, rule, cache) (filterop.hpp:48-60): nodes z_k = zr+i zi and
+   weights w_k in ascending k (ContourRule, contour.hpp:34-40). */
+int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr, const double* zi,
+                     const double* wr, const double* wi, int cache_factorizations,
+                     fl_filter** out, fl_err* err);
+int fl_filter_destroy(fl_filter* f);
+/* Y = sum_k Re(w_k (z_k I - A)^{-1} X), ascending k; FilterApplier::apply
+   (filterop.cpp:62-84). accounting counters are incremented like
+   SolveAccounting (filterop.hpp:15-18). */
+int fl_filter_apply(fl_filter* f, const fl_block* X, fl_block* Y, long long* rhs_solved,
+                    long long* factorizations, fl_err* err);
+/* same on raw buffers (host or device, per loc) */
+int fl_filter_apply_raw(fl_filter* f, const double* X, int ldx, int p, double* Y, int ldy, int loc,
+                        long long* rhs_solved, long long* factorizations, fl_err* err);
+
+/* ------------------------------------------------------------ Rayleigh-Ritz (ritz.hpp:39-57) */
+/* orthonormalize (ritz.cpp:17-59); method 0 = svd (Gram), 1 = qr */
+int fl_orthonormalize(fl_ctx* ctx, const fl_block* X, double drop_tol, int method, fl_block* U,
+                      int* rank, fl_err* err);
+/* rayleigh_ritz (ritz.cpp:83-118): host outputs vals[p], norms[p], inside[p]; V on device */
+int fl_rayleigh_ritz(fl_ctx* ctx, const fl_matrix* A, const fl_block* X, double lo, double hi,
+                     double* vals, fl_block* V, double* norms, unsigned char* inside, fl_err* err);
+/* compute_residual_block (ritz.cpp:120-122) */
+int fl_residual_block(fl_ctx* ctx, const fl_matrix* A, const fl_block* V, const double* vals,
+                      fl_block* R, fl_err* err);
+/* rank of X under ColPivHouseholderQR-style threshold (make_initial_guess, drivers.cpp:33-36) */
+int fl_block_rank(fl_ctx* ctx, const fl_block* X, double threshold, int* rank, fl_err* err);
+/* device symmetric eigensolve (SelfAdjointEigenSolver stand-in; test hook) */
+int fl_sym_eig(fl_ctx* ctx, const double* M, int p, int ldm, double* vals, double* V, int ldv,
+               fl_err* err);
+/* NodeFactorization(A, z).solve(B) (filterop.cpp:9-32; test hook): interleaved complex */
+int fl_node_solve(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, const double* B, int p,
+                  double* W, fl_err* err);
+
+/* ------------------------------------------------------------ host-level entry points
+   (the drop-in C++ layer, exported for foreign callers) */
+typedef struct fl_solver_config { /* SolverConfig, drivers.hpp:12-24 */
+  int m0;
+  int n_c;
+  int s;
+  double tol;
+  int max_iter;
+  uint64_t seed;
+  int orthogonalizer; /* 0 svd, 1 qr */
+  double drop_tol;
+  int cache_factorizations;
+  int generalized_reduced;
+} fl_solver_config;
+
+typedef struct fl_trace_record { /* TraceRecord, drivers.hpp:26-32 */
+  int iter;
+  int subspace_dim;
+  long long rhs_cumulative;
+  double max_residual;
+  int m_found;
+} fl_trace_record;
+
+/* feast_solve / xfeast_solve / rfeast_solve (drivers.hpp:58-69); variant 0/1/2.
+   Capacities: values/norms m0, vectors n*m0 (ld n), trace max_iter,
+   first_filtered n*m0 (optional, may be NULL: the first filtered block Y_1). */
+int fl_solve(fl_ctx* ctx, int variant, const double* A, int n, int lda, double lo, double hi,
+             const fl_solver_config* cfg, double* values, double* vectors, double* norms, int* m,
+             int* converged, int* iterations, long long* rhs_solved, long long* factorizations,
+             int* recovery_events, fl_trace_record* trace, int* ntrace, double* first_filtered,
+             fl_err* err);
+/* contour.hpp:28-56 */
+int fl_gauss_legendre(int n, double* nodes, double* weights, fl_err* err);
+int fl_build_contour_rule(double lo, double hi, int n_c, double* zr, double* zi, double* wr,
+                          double* wi, fl_err* err);
+double fl_filter_value(int n_c, const double* zr, const double* zi, const double* wr,
+                       const double* wi, double lambda);
+/* SymmetricMatrix ctor (matmodel.cpp:10-19) */
+int fl_symmetric_matrix(const double* M, int n, int ldm, double sym_tol, double* out, fl_err* err);
+/* make_initial_guess (drivers.cpp:23-38) — mt19937_64 + normal_distribution */
+int fl_make_initial_guess(fl_ctx* ctx, int n, int m0, uint64_t seed, double* X, fl_err* err);
+/* select_pairs ordering (ritz.cpp:124-151): chosen[0..*nchosen-1] */
+int fl_select_pairs(const double* vals, const double* norms, const unsigned char* inside, int p,
+                    int m0, double lo, double hi, int* chosen, int* nchosen, fl_err* err);
+/* seeded column-major N(0,1) / U[lo,hi) fills (fixture generation) */
+void fl_gaussian_fill(double* out, long long count, uint64_t seed);
+void fl_uniform_fill(double* out, long long count, double lo, double hi, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEASTLAB_B200_H */

@@ -175,6 +175,9 @@ class ContourRule:
     def num_points(self):
         return len(self.nodes)
 
+    def parts(self):
+        return self._parts()
+
     def _parts(self):
         z = np.ascontiguousarray(self.nodes, dtype=np.complex128)
         w = np.ascontiguousarray(self.weights, dtype=np.complex128)

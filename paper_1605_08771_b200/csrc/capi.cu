@@ -1,0 +1,1024 @@
+// Device-side implementation of the C ABI (include/feastlab_b200.h): contexts,
+// device-resident matrices and blocks, the filter orchestration
+// (FilterApplier::apply, proj/src/filterop.cpp:62-84) and the Rayleigh-Ritz
+// sequence (proj/src/ritz.cpp:17-122) on the sm_100a kernels.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/feastlab_b200.h"
+#include "common.cuh"
+#include "kernels.hpp"
+#include "ritz_kernels.hpp"
+
+namespace fl {
+std::atomic<long long> g_launch_count{0};
+}
+
+namespace {
+
+using namespace fl;
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+struct Fail {
+    int code;
+    std::string msg;
+    int index = -1;
+    double pivot = 0, zr = 0, zi = 0;
+};
+
+int report(fl_err* e, const Fail& f) {
+    if (e) {
+        e->status = f.code;
+        e->index = f.index;
+        e->pivot = f.pivot;
+        e->z_re = f.zr;
+        e->z_im = f.zi;
+        std::snprintf(e->msg, sizeof(e->msg), "%s", f.msg.c_str());
+    }
+    return f.code;
+}
+
+void cuda_check(cudaError_t c, const char* what) {
+    if (c != cudaSuccess) {
+        if (c == cudaErrorMemoryAllocation)
+            throw Fail{FL_OOM, std::string(what) + ": " + cudaGetErrorString(c)};
+        throw Fail{FL_CUDA, std::string(what) + ": " + cudaGetErrorString(c)};
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Fail{FL_NCCL, std::string(what) + ": " + ncclGetErrorString(r)};
+}
+
+// device allocation with RAII
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        CK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    double* d() const { return static_cast<double*>(p); }
+    int* i() const { return static_cast<int*>(p); }
+};
+
+}  // namespace
+
+struct fl_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    std::recursive_mutex mu;
+    long long launches_at_create = 0;
+    // Rayleigh-Ritz scratch
+    DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
+        scal;
+};
+
+struct fl_matrix {
+    fl_ctx* ctx;
+    int n, N;
+    DBuf buf;
+    double* d() const { return buf.d(); }
+};
+
+struct fl_block {
+    fl_ctx* ctx;
+    int n, N;
+    int cols = 0, cap = 0, CAP = 0;
+    int dirty = 0;  // columns [cols, dirty) may hold stale data
+    DBuf buf;
+    double* d() const { return buf.d(); }
+    long ld() const { return N; }
+};
+
+struct fl_filter {
+    fl_ctx* ctx;
+    const fl_matrix* A;
+    int nc;
+    std::vector<double> zr, zi, wr, wi;
+    bool cache;
+    int kb = 0, ke = 0;  // local node range [kb, ke)
+    // factors: cache -> one per local node; else a rotating group
+    DBuf fac_re, fac_im, ipiv, perm, bad;
+    int fac_slots = 0;
+    std::vector<char> factored;  // cache mode, per local node
+    DBuf w_re, w_im;             // W for all local nodes (N x P each)
+    long w_stride = 0;
+    int w_P = 0;
+    DBuf y_tmp;
+};
+
+namespace {
+
+struct CtxLock {
+    std::lock_guard<std::recursive_mutex> lk;
+    explicit CtxLock(fl_ctx* c) : lk(c->mu) { cudaSetDevice(c->device); }
+};
+
+void zero_cols(fl_block* b, int from, int to) {
+    if (to > from)
+        CK(cudaMemsetAsync(b->d() + (long)from * b->ld(), 0,
+                           sizeof(double) * (size_t)b->ld() * (to - from), b->ctx->stream));
+}
+
+void block_set_cols(fl_block* b, int k) {
+    // invariant: columns [cols, CAP) are zero
+    if (b->dirty > k) zero_cols(b, k, b->dirty);
+    b->cols = k;
+    b->dirty = k;
+}
+
+void block_reserve(fl_block* b, int cap) {
+    if (cap <= b->cap) return;
+    const int CAP = round_up(std::max(cap, 1), FL_TILE);
+    DBuf nb;
+    nb.ensure(sizeof(double) * (size_t)b->N * CAP);
+    CK(cudaMemsetAsync(nb.p, 0, sizeof(double) * (size_t)b->N * CAP, b->ctx->stream));
+    if (b->cols > 0)
+        CK(cudaMemcpyAsync(nb.p, b->buf.p, sizeof(double) * (size_t)b->N * b->cols,
+                           cudaMemcpyDeviceToDevice, b->ctx->stream));
+    std::swap(b->buf.p, nb.p);
+    std::swap(b->buf.bytes, nb.bytes);
+    b->cap = cap;
+    b->CAP = CAP;
+    b->dirty = b->cols;
+}
+
+void copy_in(fl_ctx* ctx, double* dst, long ldd, int n, const double* src, long lds, int p,
+             int loc) {
+    if (p <= 0 || n <= 0) return;
+    CK(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds, sizeof(double) * n,
+                         p, loc == FL_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         ctx->stream));
+}
+
+void copy_out(fl_ctx* ctx, double* dst, long ldd, int n, const double* src, long lds, int p,
+              int loc) {
+    if (p <= 0 || n <= 0) return;
+    CK(cudaMemcpy2DAsync(dst, sizeof(double) * ldd, src, sizeof(double) * lds, sizeof(double) * n,
+                         p, loc == FL_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         ctx->stream));
+}
+
+void sync(fl_ctx* ctx) { CK(cudaStreamSynchronize(ctx->stream)); }
+
+// --------------------------------------------------------------- filter core
+// Factor nodes [g0, g0+G) of the local range into factor slots [s0, s0+G).
+void factor_group(fl_filter* f, int g0, int G, int s0) {
+    fl_ctx* ctx = f->ctx;
+    const int N = f->A->N, n = f->A->n;
+    const long stride = (long)N * N;
+    ZBatch F{f->fac_re.d() + s0 * stride, f->fac_im.d() + s0 * stride, N, stride};
+    NodeShifts z{};
+    for (int b = 0; b < G; ++b) {
+        z.zr[b] = f->zr[f->kb + g0 + b];
+        z.zi[b] = f->zi[f->kb + g0 + b];
+    }
+    int* ipiv = f->ipiv.i() + (long)s0 * N;
+    launch_shift(f->A->d(), N, N, F, z, G, ctx->stream);
+    g_launch_count += 1;
+    for (int k0 = 0; k0 < N; k0 += FL_TILE) {
+        launch_panel(F, N, k0, ipiv, G, ctx->stream);
+        launch_laswp_panel(F, N, k0, ipiv, G, ctx->stream);
+        g_launch_count += 2;
+        const int rest = N - k0 - FL_TILE;
+        if (rest > 0) {
+            launch_trsm_unit_lower(F, k0, F, k0, k0 + FL_TILE, rest, G, ctx->stream);
+            ZGemm g{rest, rest, FL_TILE,
+                    F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N, stride,
+                    F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0, N, stride,
+                    F.re + (long)(k0 + FL_TILE) * N + k0 + FL_TILE,
+                    F.im + (long)(k0 + FL_TILE) * N + k0 + FL_TILE, N, stride};
+            launch_zgemm_sub(g, G, ctx->stream);
+            g_launch_count += 2;
+        }
+    }
+    launch_check_diag(F, n, G, g0, f->bad.i(), ctx->stream);
+    launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, ctx->stream);
+    g_launch_count += 2;
+}
+
+// W_b = (z_b I - A)^{-1} X for nodes [g0, g0+G) using factor slots [s0, ...).
+void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx, int P) {
+    fl_ctx* ctx = f->ctx;
+    const int N = f->A->N;
+    const long stride = (long)N * N;
+    ZBatch F{f->fac_re.d() + s0 * stride, f->fac_im.d() + s0 * stride, N, stride};
+    ZBatch W{f->w_re.d() + g0 * f->w_stride, f->w_im.d() + g0 * f->w_stride, N, f->w_stride};
+    launch_permute_rhs(X, ldx, N, P, f->perm.i() + (long)s0 * N, W, G, ctx->stream);
+    g_launch_count += 1;
+    const int NB = N / FL_TILE;
+    for (int ib = 0; ib < NB; ++ib) {  // forward, unit lower
+        const int r0 = ib * FL_TILE;
+        launch_trsm_unit_lower(F, r0, W, r0, 0, P, G, ctx->stream);
+        const int rest = N - r0 - FL_TILE;
+        g_launch_count += 1;
+        if (rest > 0) {
+            ZGemm g{rest, P, FL_TILE,
+                    F.re + (long)r0 * N + r0 + FL_TILE, F.im + (long)r0 * N + r0 + FL_TILE, N, stride,
+                    W.re + r0, W.im + r0, N, W.stride,
+                    W.re + r0 + FL_TILE, W.im + r0 + FL_TILE, N, W.stride};
+            launch_zgemm_sub(g, G, ctx->stream);
+            g_launch_count += 1;
+        }
+    }
+    for (int ib = NB - 1; ib >= 0; --ib) {  // backward, upper
+        const int r0 = ib * FL_TILE;
+        launch_trsm_upper(F, r0, W, r0, 0, P, G, ctx->stream);
+        g_launch_count += 1;
+        if (r0 > 0) {
+            ZGemm g{r0, P, FL_TILE,
+                    F.re + (long)r0 * N, F.im + (long)r0 * N, N, stride,
+                    W.re + r0, W.im + r0, N, W.stride,
+                    W.re, W.im, N, W.stride};
+            launch_zgemm_sub(g, G, ctx->stream);
+            g_launch_count += 1;
+        }
+    }
+}
+
+size_t free_bytes() {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    return fr;
+}
+
+// X, Y: device, N x P padded (zero rows >= n, zero cols >= p); P multiple of 64.
+void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y, long ldy,
+                      long long* rhs, long long* facts) {
+    fl_ctx* ctx = f->ctx;
+    const int N = f->A->N;
+    const int P = round_up(p, FL_TILE);
+    const int L = f->ke - f->kb;
+    const long fstride = (long)N * N;
+    // W for every local node
+    if (f->w_P < P || f->w_stride != (long)N * P) {
+        f->w_stride = (long)N * P;
+        f->w_re.ensure(sizeof(double) * (size_t)f->w_stride * std::max(L, 1));
+        f->w_im.ensure(sizeof(double) * (size_t)f->w_stride * std::max(L, 1));
+        f->w_P = P;
+    }
+    // factor slots
+    int slots;
+    if (f->cache) {
+        slots = L;
+    } else {
+        const size_t per = sizeof(double) * 2 * (size_t)fstride + sizeof(int) * 2 * (size_t)N;
+        const size_t budget = (size_t)(0.6 * (double)(free_bytes() + f->fac_re.bytes + f->fac_im.bytes));
+        slots = (int)std::max<size_t>(1, std::min<size_t>((size_t)L, budget / per));
+        slots = std::min(slots, 16);
+    }
+    if (f->fac_slots < slots) {
+        f->fac_re.release();
+        f->fac_im.release();
+        f->fac_re.ensure(sizeof(double) * (size_t)fstride * slots);
+        f->fac_im.ensure(sizeof(double) * (size_t)fstride * slots);
+        f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
+        f->perm.ensure(sizeof(int) * (size_t)N * slots);
+        f->fac_slots = slots;
+        std::fill(f->factored.begin(), f->factored.end(), 0);
+    }
+    f->bad.ensure(sizeof(int) * 4);
+    int big = 0x7fffffff;
+    CK(cudaMemcpyAsync(f->bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    long long new_facts = 0;
+    if (f->cache) {
+        // factor the not-yet-cached nodes in contiguous runs
+        int g = 0;
+        while (g < L) {
+            if (f->factored[g]) { ++g; continue; }
+            int e = g;
+            while (e < L && !f->factored[e] && e - g < 16) ++e;
+            factor_group(f, g, e - g, g);
+            // slot-relative bad index -> local node index
+            for (int k = g; k < e; ++k) f->factored[k] = 1;
+            new_facts += e - g;
+            g = e;
+        }
+        solve_group(f, 0, L, 0, X, ldx, P);
+    } else {
+        for (int g = 0; g < L; g += slots) {
+            const int G = std::min(slots, L - g);
+            // bad index is relative to the group; offset by shifting the flag base
+            factor_group(f, g, G, 0);
+            int h_bad = 0;
+            CK(cudaMemcpyAsync(&h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+            if (h_bad != 0x7fffffff) {
+                const int k = f->kb + h_bad;
+                if (facts) *facts += h_bad;  // nodes factored before it (filterop.cpp:74-76)
+                char buf[256];
+                std::snprintf(buf, sizeof(buf),
+                              "factorize_node: singular factorization at node %d (z = %f+%fi)", k,
+                              f->zr[k], f->zi[k]);
+                Fail fl{FL_SINGULAR_NODE, buf};
+                fl.index = k;
+                fl.zr = f->zr[k];
+                fl.zi = f->zi[k];
+                throw fl;
+            }
+            solve_group(f, g, G, 0, X, ldx, P);
+        }
+        new_facts = f->nc;
+    }
+    if (f->cache) {
+        int h_bad = 0;
+        CK(cudaMemcpyAsync(&h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        if (h_bad != 0x7fffffff) {
+            const int k = f->kb + h_bad;
+            std::fill(f->factored.begin(), f->factored.end(), 0);
+            char buf[256];
+            std::snprintf(buf, sizeof(buf),
+                          "factorize_node: singular factorization at node %d (z = %f+%fi)", k,
+                          f->zr[k], f->zi[k]);
+            Fail fl{FL_SINGULAR_NODE, buf};
+            fl.index = k;
+            fl.zr = f->zr[k];
+            fl.zi = f->zi[k];
+            throw fl;
+        }
+        if (ctx->nranks > 1) {
+            // factorizations are counted globally: every rank adds the same total
+            long long loc = new_facts, tot = 0;
+            DBuf t;
+            t.ensure(sizeof(long long));
+            CK(cudaMemcpyAsync(t.p, &loc, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+            nccl_check(ncclAllReduce(t.p, t.p, 1, ncclInt64, ncclSum, ctx->comm, ctx->stream),
+                       "ncclAllReduce(facts)");
+            CK(cudaMemcpyAsync(&tot, t.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+            sync(ctx);
+            new_facts = tot;
+        }
+    }
+    // ordered accumulation over the local nodes
+    NodeShifts w{};
+    for (int b = 0; b < L; ++b) {
+        w.zr[b] = f->wr[f->kb + b];
+        w.zi[b] = f->wi[f->kb + b];
+    }
+    ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
+    if (L > 0) {
+        launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
+        g_launch_count += 1;
+    } else {
+        CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
+    }
+    if (ctx->nranks > 1) {
+        if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
+        nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm, ctx->stream),
+                   "ncclAllReduce(Y)");
+    }
+    if (rhs) *rhs += (long long)f->nc * p;
+    if (facts) *facts += new_facts;
+}
+
+// --------------------------------------------------------------- Rayleigh-Ritz helpers
+double* scratch(DBuf& b, size_t doubles) {
+    b.ensure(sizeof(double) * std::max<size_t>(doubles, 1));
+    return b.d();
+}
+
+// Symmetric eigensolve of the p x p matrix M (device, ld ldm, destroyed):
+// ascending vals (device), vectors into V (P x P zero-padded, ld P).
+void device_sym_eig(fl_ctx* ctx, double* M, long ldm, int p, int P, double* vals, double* V,
+                    double* work, double* Vtmp) {
+    launch_fro2(M, ldm, p, ctx->scal.d(), ctx->stream);
+    double fro2 = 0.0;
+    CK(cudaMemcpyAsync(&fro2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    CK(cudaMemsetAsync(V, 0, sizeof(double) * (size_t)P * P, ctx->stream));
+    CK(cudaMemsetAsync(Vtmp, 0, sizeof(double) * (size_t)P * P, ctx->stream));
+    const int rc = jacobi_eig(M, ldm, p, std::sqrt(fro2), work, Vtmp, P, vals, V, P,
+                              ctx->ints.i(), reinterpret_cast<unsigned long long*>(ctx->cnt.p), 40,
+                              ctx->stream);
+    g_launch_count += 4;
+    if (rc != 0) throw Fail{FL_CUDA, "jacobi_eig: cooperative launch failed"};
+    CK(cudaGetLastError());
+}
+
+void ensure_rr_scratch(fl_ctx* ctx) {
+    ctx->chol_info.ensure(64);
+    ctx->ints.ensure(64);
+    ctx->cnt.ensure(sizeof(unsigned long long) * 64);
+    ctx->scal.ensure(64);
+}
+
+void orthonormalize_dev(fl_ctx* ctx, const fl_block* X, double drop_tol, fl_block* U, int* rank_out) {
+    const int p = X->cols, N = X->N, n = X->n;
+    if (p < 1 || n < 1) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: empty block"};
+    const int P = round_up(p, FL_TILE);
+    ensure_rr_scratch(ctx);
+    double* G = scratch(ctx->s1, (size_t)P * P);
+    double* Gs = scratch(ctx->s2, (size_t)P * P);
+    double* work = scratch(ctx->s3, (size_t)P * P);
+    double* V = scratch(ctx->s4, (size_t)P * P);
+    double* Vt = scratch(ctx->s5, (size_t)P * P);
+    double* vals = scratch(ctx->vals_d, P);
+    // G = X^T X (ritz.cpp:32), symmetrised (:33)
+    DGemm g{P, P, N, X->d(), X->ld(), 0, X->d(), X->ld(), 0, G, P, 0, 1.0, 0.0};
+    launch_dgemm(g, true, false, 1, ctx->stream);
+    launch_symmetrize(G, P, p, Gs, P, ctx->stream);
+    g_launch_count += 2;
+    device_sym_eig(ctx, Gs, P, p, P, vals, V, work, Vt);  // ascending (:34-35)
+    std::vector<double> ev(p);
+    CK(cudaMemcpyAsync(ev.data(), vals, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    // host decision logic, verbatim (ritz.cpp:36-51)
+    const double sigma_max = std::sqrt(std::max(0.0, ev[p - 1]));
+    if (!(sigma_max > 0.0)) throw Fail{FL_RUNTIME_ERROR, "orthonormalize: block is numerically zero"};
+    const double ev_floor =
+        std::max(drop_tol * drop_tol, std::numeric_limits<double>::epsilon() * p) * ev[p - 1];
+    std::vector<int> keep;
+    for (int i = p - 1; i >= 0; --i)
+        if (ev[i] > ev_floor) keep.push_back(i);
+    const int rank = (int)keep.size();
+    if (rank == 0) throw Fail{FL_RUNTIME_ERROR, "orthonormalize: block is numerically zero"};
+    const int RP = round_up(rank, FL_TILE);
+    // Vk = V[:, keep] (zero padded), U = X Vk, U[:, j] /= sigma_j (:53-57)
+    std::vector<double> sig(rank);
+    for (int j = 0; j < rank; ++j) sig[j] = std::sqrt(ev[keep[j]]);
+    int* idx = reinterpret_cast<int*>(scratch(ctx->idx_d, rank));
+    double* sg = scratch(ctx->norms_d, rank);
+    CK(cudaMemcpyAsync(idx, keep.data(), sizeof(int) * rank, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(sg, sig.data(), sizeof(double) * rank, cudaMemcpyHostToDevice, ctx->stream));
+    double* Vk = Vt;  // reuse
+    launch_gather_cols(V, P, P, idx, rank, RP, Vk, P, ctx->stream);
+    block_reserve(U, rank);
+    block_set_cols(U, rank);
+    DGemm h{N, RP, P, X->d(), X->ld(), 0, Vk, P, 0, U->d(), U->ld(), 0, 1.0, 0.0};
+    launch_dgemm(h, false, false, 1, ctx->stream);
+    launch_col_div(U->d(), U->ld(), n, rank, sg, ctx->stream);
+    g_launch_count += 3;
+    U->dirty = std::max(U->dirty, RP);
+    block_set_cols(U, rank);
+    sync(ctx);  // host vectors (keep, sig) go out of scope
+    *rank_out = rank;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ M, long ldm, int P, double* T, long ldt) {
+    const long total = (long)P * P;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / P), i = (int)(e - (long)j * P);
+        T[(long)j * ldt + i] = M[(long)i * ldm + j];
+    }
+}
+
+struct RRResult {
+    std::vector<double> vals, norms;
+    std::vector<unsigned char> inside;
+};
+
+void rayleigh_ritz_dev(fl_ctx* ctx, const fl_matrix* A, const fl_block* X, double lo, double hi,
+                       fl_block* Vout, RRResult& out) {
+    const int p = X->cols, N = X->N, n = X->n;
+    if (n != A->n) throw Fail{FL_INVALID_ARGUMENT, "rayleigh_ritz: block/matrix dimension mismatch"};
+    if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "rayleigh_ritz: empty block"};
+    const int P = round_up(p, FL_TILE);
+    ensure_rr_scratch(ctx);
+    double* AX = scratch(ctx->rr_nxp, (size_t)N * P);
+    double* Ap = scratch(ctx->s1, (size_t)P * P);
+    double* Bp = scratch(ctx->s2, (size_t)P * P);
+    double* Aps = scratch(ctx->s3, (size_t)P * P);
+    double* L = scratch(ctx->s4, (size_t)P * P);
+    double* C = scratch(ctx->s5, (size_t)P * P);
+    double* V = scratch(ctx->s6, (size_t)P * P);
+    double* Vt = scratch(ctx->s7, (size_t)P * P);
+    double* vals = scratch(ctx->vals_d, P);
+    double* nrm = scratch(ctx->norms_d, P);
+    cudaStream_t s = ctx->stream;
+    // AX = A X ; A' = X^T AX ; B' = X^T X (ritz.cpp:90-92)
+    launch_dgemm(DGemm{N, P, N, A->d(), N, 0, X->d(), X->ld(), 0, AX, N, 0, 1.0, 0.0}, false, false, 1, s);
+    launch_dgemm(DGemm{P, P, N, X->d(), X->ld(), 0, AX, N, 0, Ap, P, 0, 1.0, 0.0}, true, false, 1, s);
+    launch_dgemm(DGemm{P, P, N, X->d(), X->ld(), 0, X->d(), X->ld(), 0, Bp, P, 0, 1.0, 0.0}, true, false, 1, s);
+    // symmetrise (:93-94) into zero-padded buffers; B' padded with identity
+    CK(cudaMemsetAsync(Aps, 0, sizeof(double) * (size_t)P * P, s));
+    CK(cudaMemsetAsync(L, 0, sizeof(double) * (size_t)P * P, s));
+    launch_symmetrize(Ap, P, p, Aps, P, s);
+    launch_symmetrize(Bp, P, p, L, P, s);
+    launch_set_diag(L, P, p, P, 1.0, s);
+    // L = chol(B') with the first failing pivot (:96, :64-79)
+    int init[4] = {-1, 0, 0, 0};
+    CK(cudaMemcpyAsync(ctx->chol_info.p, init, 16, cudaMemcpyHostToDevice, s));
+    launch_cholesky(L, P, p, P, ctx->chol_info.p, s);
+    struct {
+        int index;
+        double pivot;
+    } info;
+    CK(cudaMemcpyAsync(&info, ctx->chol_info.p, sizeof(info), cudaMemcpyDeviceToHost, s));
+    sync(ctx);
+    g_launch_count += 8 + 3 * (P / 64);
+    if (info.index >= 0) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "rayleigh_ritz: B' not numerically SPD, pivot %f at index %d",
+                      info.pivot, info.index);
+        Fail f{FL_CHOLESKY, buf};
+        f.index = info.index;
+        f.pivot = info.pivot;
+        throw f;
+    }
+    launch_tril(L, P, P, s);
+    // T = L^{-1} A' (:97) ; C = L^{-1} T^T (:98) ; symmetrise (:99)
+    launch_trsm_lower(L, P, P, Aps, P, P, false, s);
+    transpose_kernel<<<148, 256, 0, s>>>(Aps, P, P, C, P);
+    launch_trsm_lower(L, P, P, C, P, P, false, s);
+    CK(cudaMemsetAsync(Ap, 0, sizeof(double) * (size_t)P * P, s));
+    launch_symmetrize(C, P, p, Ap, P, s);
+    g_launch_count += 3 + 4 * (P / 64);
+    // eig (:101), Q = L^{-T} V (:102-103)
+    device_sym_eig(ctx, Ap, P, p, P, vals, V, C, Vt);
+    launch_trsm_lower(L, P, P, V, P, P, true, s);
+    // vectors = X Q (:107)
+    block_reserve(Vout, p);
+    block_set_cols(Vout, p);
+    launch_dgemm(DGemm{N, P, P, X->d(), X->ld(), 0, V, P, 0, Vout->d(), Vout->ld(), 0, 1.0, 0.0},
+                 false, false, 1, s);
+    Vout->dirty = std::max(Vout->dirty, P);
+    block_set_cols(Vout, p);
+    // unit-normalise (:110-112)
+    launch_col_norms(Vout->d(), Vout->ld(), n, p, nrm, s);
+    launch_col_div(Vout->d(), Vout->ld(), n, p, nrm, s);
+    // R = A V - V diag(lam) (:115), norms (:116)
+    launch_dgemm(DGemm{N, P, N, A->d(), N, 0, Vout->d(), Vout->ld(), 0, AX, N, 0, 1.0, 0.0}, false,
+                 false, 1, s);
+    double* R = scratch(ctx->rr_nxp2, (size_t)N * P);
+    launch_residual(AX, N, Vout->d(), Vout->ld(), n, p, vals, R, N, s);
+    launch_col_norms(R, N, n, p, nrm, s);
+    g_launch_count += 7 + 2 * (P / 64);
+    out.vals.resize(p);
+    out.norms.resize(p);
+    out.inside.resize(p);
+    CK(cudaMemcpyAsync(out.vals.data(), vals, sizeof(double) * p, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out.norms.data(), nrm, sizeof(double) * p, cudaMemcpyDeviceToHost, s));
+    sync(ctx);
+    for (int k = 0; k < p; ++k) out.inside[k] = (out.vals[k] > lo && out.vals[k] < hi) ? 1 : 0;
+}
+
+template <class F>
+int guarded(fl_err* err, F&& body) {
+    try {
+        body();
+        return FL_OK;
+    } catch (const Fail& f) {
+        return report(err, f);
+    } catch (const std::bad_alloc&) {
+        return report(err, Fail{FL_OOM, "host allocation failed"});
+    } catch (const std::exception& e) {
+        return report(err, Fail{FL_RUNTIME_ERROR, e.what()});
+    }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int fl_version(void) { return 1; }
+
+int fl_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    *count = (e == cudaSuccess) ? c : 0;
+    return e == cudaSuccess ? FL_OK : FL_CUDA;
+}
+
+static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_ctx** out,
+                           fl_err* err) {
+    return guarded(err, [&] {
+        int cnt = 0;
+        if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+            throw Fail{FL_CUDA, "no CUDA device: the feastlab B200 path has no CPU fallback"};
+        if (device < 0 || device >= cnt) throw Fail{FL_INVALID_ARGUMENT, "bad device index"};
+        std::unique_ptr<fl_ctx> c(new fl_ctx());
+        c->device = device;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->rank = rank;
+        c->nranks = nranks;
+        if (nranks > 1) {
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, sizeof(uid));
+            nccl_check(ncclCommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+        }
+        c->launches_at_create = g_launch_count.load();
+        *out = c.release();
+    });
+}
+
+int fl_ctx_create(int device, fl_ctx** out, fl_err* err) {
+    return ctx_create_impl(device, nullptr, 0, 1, out, err);
+}
+
+int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl_ctx** out,
+                       fl_err* err) {
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return report(err, Fail{FL_INVALID_ARGUMENT, "bad rank/nranks"});
+    return ctx_create_impl(device, nccl_id, rank, nranks, out, err);
+}
+
+int fl_nccl_unique_id(void* out128, fl_err* err) {
+    return guarded(err, [&] {
+        ncclUniqueId uid;
+        nccl_check(ncclGetUniqueId(&uid), "ncclGetUniqueId");
+        std::memcpy(out128, &uid, sizeof(uid));
+    });
+}
+
+int fl_ctx_destroy(fl_ctx* ctx) {
+    if (!ctx) return FL_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return FL_OK;
+}
+
+int fl_ctx_sync(fl_ctx* ctx, fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        sync(ctx);
+    });
+}
+
+void* fl_ctx_stream(fl_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
+    *rank = ctx->rank;
+    *nranks = ctx->nranks;
+    return FL_OK;
+}
+
+long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
+
+int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_matrix** out,
+                     fl_err* err) {
+    return guarded(err, [&] {
+        if (n < 1 || lda < n) throw Fail{FL_INVALID_ARGUMENT, "fl_matrix_create: bad shape"};
+        CtxLock lk(ctx);
+        std::unique_ptr<fl_matrix> m(new fl_matrix());
+        m->ctx = ctx;
+        m->n = n;
+        m->N = round_up(n, FL_TILE);
+        m->buf.ensure(sizeof(double) * (size_t)m->N * m->N);
+        CK(cudaMemsetAsync(m->buf.p, 0, sizeof(double) * (size_t)m->N * m->N, ctx->stream));
+        copy_in(ctx, m->d(), m->N, n, A, lda, n, loc);
+        sync(ctx);
+        *out = m.release();
+    });
+}
+
+int fl_matrix_destroy(fl_matrix* m) {
+    if (m) {
+        cudaSetDevice(m->ctx->device);
+        delete m;
+    }
+    return FL_OK;
+}
+
+int fl_matrix_dim(const fl_matrix* m) { return m->n; }
+
+int fl_block_create(fl_ctx* ctx, int n, int cap_cols, fl_block** out, fl_err* err) {
+    return guarded(err, [&] {
+        if (n < 1 || cap_cols < 0) throw Fail{FL_INVALID_ARGUMENT, "fl_block_create: bad shape"};
+        CtxLock lk(ctx);
+        std::unique_ptr<fl_block> b(new fl_block());
+        b->ctx = ctx;
+        b->n = n;
+        b->N = round_up(n, FL_TILE);
+        block_reserve(b.get(), std::max(cap_cols, 1));
+        *out = b.release();
+    });
+}
+
+int fl_block_destroy(fl_block* b) {
+    if (b) {
+        cudaSetDevice(b->ctx->device);
+        delete b;
+    }
+    return FL_OK;
+}
+
+int fl_block_cols(const fl_block* b) { return b->cols; }
+int fl_block_rows(const fl_block* b) { return b->n; }
+
+int fl_block_set(fl_block* b, const double* X, int ldx, int p, int loc, fl_err* err) {
+    return guarded(err, [&] {
+        if (p < 0 || ldx < b->n) throw Fail{FL_INVALID_ARGUMENT, "fl_block_set: bad shape"};
+        CtxLock lk(b->ctx);
+        block_reserve(b, p);
+        block_set_cols(b, p);
+        copy_in(b->ctx, b->d(), b->ld(), b->n, X, ldx, p, loc);
+        if (loc == FL_HOST) sync(b->ctx);
+    });
+}
+
+int fl_block_get(const fl_block* b, double* X, int ldx, int loc, fl_err* err) {
+    return guarded(err, [&] {
+        if (ldx < b->n) throw Fail{FL_INVALID_ARGUMENT, "fl_block_get: bad ld"};
+        CtxLock lk(b->ctx);
+        copy_out(b->ctx, X, ldx, b->n, b->d(), b->ld(), b->cols, loc);
+        if (loc == FL_HOST) sync(b->ctx);
+    });
+}
+
+int fl_block_gather(fl_block* dst, const fl_block* src, const int* idx, int k, fl_err* err) {
+    return guarded(err, [&] {
+        if (dst == src) throw Fail{FL_INVALID_ARGUMENT, "fl_block_gather: dst aliases src"};
+        if (dst->n != src->n) throw Fail{FL_INVALID_ARGUMENT, "fl_block_gather: row mismatch"};
+        for (int j = 0; j < k; ++j)
+            if (idx[j] < 0 || idx[j] >= src->cols)
+                throw Fail{FL_INVALID_ARGUMENT, "fl_block_gather: index out of range"};
+        fl_ctx* ctx = dst->ctx;
+        CtxLock lk(ctx);
+        block_reserve(dst, k);
+        int* d_idx = reinterpret_cast<int*>(scratch(ctx->idx_d, std::max(k, 1)));
+        if (k > 0)
+            CK(cudaMemcpyAsync(d_idx, idx, sizeof(int) * k, cudaMemcpyHostToDevice, ctx->stream));
+        const int kp = round_up(std::max(k, 1), FL_TILE);
+        launch_gather_cols(src->d(), src->ld(), src->N, d_idx, k, std::min(kp, dst->CAP), dst->d(),
+                           dst->ld(), ctx->stream);
+        g_launch_count += 1;
+        dst->dirty = std::max(dst->dirty, std::min(kp, dst->CAP));
+        block_set_cols(dst, k);
+        sync(ctx);
+    });
+}
+
+int fl_block_append(fl_block* dst, const fl_block* src, fl_err* err) {
+    return guarded(err, [&] {
+        if (dst->n != src->n) throw Fail{FL_INVALID_ARGUMENT, "fl_block_append: row mismatch"};
+        CtxLock lk(dst->ctx);
+        const int c0 = dst->cols, k = src->cols;
+        block_reserve(dst, c0 + k);
+        if (k > 0)
+            CK(cudaMemcpyAsync(dst->d() + (long)c0 * dst->ld(), src->d(),
+                               sizeof(double) * (size_t)dst->ld() * k, cudaMemcpyDeviceToDevice,
+                               dst->ctx->stream));
+        dst->cols = c0 + k;
+        dst->dirty = std::max(dst->dirty, dst->cols);
+    });
+}
+
+int fl_block_copy(fl_block* dst, const fl_block* src, fl_err* err) {
+    return guarded(err, [&] {
+        if (dst->n != src->n) throw Fail{FL_INVALID_ARGUMENT, "fl_block_copy: row mismatch"};
+        if (dst == src) return;
+        CtxLock lk(dst->ctx);
+        block_reserve(dst, src->cols);
+        block_set_cols(dst, src->cols);
+        if (src->cols > 0)
+            CK(cudaMemcpyAsync(dst->d(), src->d(), sizeof(double) * (size_t)dst->ld() * src->cols,
+                               cudaMemcpyDeviceToDevice, dst->ctx->stream));
+    });
+}
+
+int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr, const double* zi,
+                     const double* wr, const double* wi, int cache, fl_filter** out, fl_err* err) {
+    return guarded(err, [&] {
+        if (n_c < 1 || n_c > kMaxNodes)
+            throw Fail{FL_INVALID_ARGUMENT, "fl_filter_create: need 1 <= n_c <= 64"};
+        std::unique_ptr<fl_filter> f(new fl_filter());
+        f->ctx = ctx;
+        f->A = A;
+        f->nc = n_c;
+        f->zr.assign(zr, zr + n_c);
+        f->zi.assign(zi, zi + n_c);
+        f->wr.assign(wr, wr + n_c);
+        f->wi.assign(wi, wi + n_c);
+        f->cache = cache != 0;
+        // contiguous node shard of this rank
+        const int R = ctx->nranks, r = ctx->rank;
+        f->kb = (int)((long)n_c * r / R);
+        f->ke = (int)((long)n_c * (r + 1) / R);
+        f->factored.assign(f->ke - f->kb, 0);
+        *out = f.release();
+    });
+}
+
+int fl_filter_destroy(fl_filter* f) {
+    if (f) {
+        cudaSetDevice(f->ctx->device);
+        delete f;
+    }
+    return FL_OK;
+}
+
+int fl_filter_apply(fl_filter* f, const fl_block* X, fl_block* Y, long long* rhs, long long* facts,
+                    fl_err* err) {
+    return guarded(err, [&] {
+        if (X->n != f->A->n)
+            throw Fail{FL_INVALID_ARGUMENT, "apply_filter: block dimension " + std::to_string(X->n) +
+                                                " != matrix dimension " + std::to_string(f->A->n)};
+        if (X->cols < 1) throw Fail{FL_INVALID_ARGUMENT, "apply_filter: block must have p >= 1"};
+        if (X == Y) throw Fail{FL_INVALID_ARGUMENT, "apply_filter: X and Y must differ"};
+        CtxLock lk(f->ctx);
+        block_reserve(Y, X->cols);
+        block_set_cols(Y, X->cols);
+        filter_apply_dev(f, X->d(), X->ld(), X->cols, Y->d(), Y->ld(), rhs, facts);
+        Y->dirty = std::max(Y->dirty, round_up(X->cols, FL_TILE));
+        block_set_cols(Y, X->cols);
+    });
+}
+
+int fl_filter_apply_raw(fl_filter* f, const double* X, int ldx, int p, double* Y, int ldy, int loc,
+                        long long* rhs, long long* facts, fl_err* err) {
+    return guarded(err, [&] {
+        const int n = f->A->n, N = f->A->N;
+        if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "apply_filter: block must have p >= 1"};
+        if (ldx < n || ldy < n) throw Fail{FL_INVALID_ARGUMENT, "apply_filter: bad leading dimension"};
+        fl_ctx* ctx = f->ctx;
+        CtxLock lk(ctx);
+        const int P = round_up(p, FL_TILE);
+        // padded staging copies (zero rows >= n, zero cols >= p)
+        double* Xs = scratch(f->y_tmp, (size_t)2 * N * P);
+        double* Ys = Xs + (size_t)N * P;
+        CK(cudaMemsetAsync(Xs, 0, sizeof(double) * (size_t)N * P, ctx->stream));
+        copy_in(ctx, Xs, N, n, X, ldx, p, loc);
+        filter_apply_dev(f, Xs, N, p, Ys, N, rhs, facts);
+        copy_out(ctx, Y, ldy, n, Ys, N, p, loc);
+        if (loc == FL_HOST) sync(ctx);
+    });
+}
+
+int fl_orthonormalize(fl_ctx* ctx, const fl_block* X, double drop_tol, int method, fl_block* U,
+                      int* rank, fl_err* err) {
+    return guarded(err, [&] {
+        if (X->cols < 1 || X->n < 1) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: empty block"};
+        if (method != 0)
+            throw Fail{FL_INVALID_ARGUMENT,
+                       "orthonormalize: the qr orthogonalizer is not implemented on the device yet"};
+        if (X == U) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: X and U must differ"};
+        CtxLock lk(ctx);
+        orthonormalize_dev(ctx, X, drop_tol, U, rank);
+    });
+}
+
+int fl_rayleigh_ritz(fl_ctx* ctx, const fl_matrix* A, const fl_block* X, double lo, double hi,
+                     double* vals, fl_block* V, double* norms, unsigned char* inside, fl_err* err) {
+    return guarded(err, [&] {
+        if (X == V) throw Fail{FL_INVALID_ARGUMENT, "rayleigh_ritz: X and V must differ"};
+        CtxLock lk(ctx);
+        RRResult r;
+        rayleigh_ritz_dev(ctx, A, X, lo, hi, V, r);
+        std::memcpy(vals, r.vals.data(), sizeof(double) * r.vals.size());
+        std::memcpy(norms, r.norms.data(), sizeof(double) * r.norms.size());
+        std::memcpy(inside, r.inside.data(), r.inside.size());
+    });
+}
+
+int fl_residual_block(fl_ctx* ctx, const fl_matrix* A, const fl_block* V, const double* vals,
+                      fl_block* R, fl_err* err) {
+    return guarded(err, [&] {
+        if (V->n != A->n) throw Fail{FL_INVALID_ARGUMENT, "compute_residual_block: dimension mismatch"};
+        if (V == R) throw Fail{FL_INVALID_ARGUMENT, "compute_residual_block: V and R must differ"};
+        CtxLock lk(ctx);
+        const int p = V->cols, N = V->N, n = V->n;
+        const int P = round_up(std::max(p, 1), FL_TILE);
+        double* AV = scratch(ctx->rr_nxp, (size_t)N * P);
+        double* lam = scratch(ctx->vals_d, P);
+        if (p > 0)
+            CK(cudaMemcpyAsync(lam, vals, sizeof(double) * p, cudaMemcpyHostToDevice, ctx->stream));
+        launch_dgemm(DGemm{N, P, N, A->d(), N, 0, V->d(), V->ld(), 0, AV, N, 0, 1.0, 0.0}, false,
+                     false, 1, ctx->stream);
+        block_reserve(R, p);
+        block_set_cols(R, p);
+        launch_residual(AV, N, V->d(), V->ld(), n, p, lam, R->d(), R->ld(), ctx->stream);
+        g_launch_count += 2;
+        sync(ctx);
+    });
+}
+
+int fl_block_rank(fl_ctx* ctx, const fl_block* X, double threshold, int* rank, fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        const int p = X->cols, N = X->N;
+        if (p < 1) {
+            *rank = 0;
+            return;
+        }
+        const int P = round_up(p, FL_TILE);
+        ensure_rr_scratch(ctx);
+        double* G = scratch(ctx->s1, (size_t)P * P);
+        double* Gs = scratch(ctx->s2, (size_t)P * P);
+        double* work = scratch(ctx->s3, (size_t)P * P);
+        double* V = scratch(ctx->s4, (size_t)P * P);
+        double* Vt = scratch(ctx->s5, (size_t)P * P);
+        double* vals = scratch(ctx->vals_d, P);
+        launch_dgemm(DGemm{P, P, N, X->d(), X->ld(), 0, X->d(), X->ld(), 0, G, P, 0, 1.0, 0.0}, true,
+                     false, 1, ctx->stream);
+        launch_symmetrize(G, P, p, Gs, P, ctx->stream);
+        device_sym_eig(ctx, Gs, P, p, P, vals, V, work, Vt);
+        std::vector<double> ev(p);
+        CK(cudaMemcpyAsync(ev.data(), vals, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        // singular values sigma_i = sqrt(ev_i); rank = #{sigma_i > threshold * sigma_max}
+        const double smax = std::sqrt(std::max(0.0, ev[p - 1]));
+        int r = 0;
+        for (int i = 0; i < p; ++i)
+            if (std::sqrt(std::max(0.0, ev[i])) > threshold * smax) ++r;
+        *rank = r;
+    });
+}
+
+int fl_sym_eig(fl_ctx* ctx, const double* M, int p, int ldm, double* vals, double* V, int ldv,
+               fl_err* err) {
+    return guarded(err, [&] {
+        if (p < 1 || ldm < p || ldv < p) throw Fail{FL_INVALID_ARGUMENT, "fl_sym_eig: bad shape"};
+        CtxLock lk(ctx);
+        const int P = round_up(p, FL_TILE);
+        ensure_rr_scratch(ctx);
+        double* Md = scratch(ctx->s1, (size_t)P * P);
+        double* work = scratch(ctx->s3, (size_t)P * P);
+        double* Vd = scratch(ctx->s4, (size_t)P * P);
+        double* Vt = scratch(ctx->s5, (size_t)P * P);
+        double* vd = scratch(ctx->vals_d, P);
+        CK(cudaMemsetAsync(Md, 0, sizeof(double) * (size_t)P * P, ctx->stream));
+        copy_in(ctx, Md, P, p, M, ldm, p, FL_HOST);
+        device_sym_eig(ctx, Md, P, p, P, vd, Vd, work, Vt);
+        CK(cudaMemcpyAsync(vals, vd, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream));
+        copy_out(ctx, V, ldv, p, Vd, P, p, FL_HOST);
+        sync(ctx);
+    });
+}
+
+int fl_node_solve(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, const double* B, int p,
+                  double* W, fl_err* err) {
+    return guarded(err, [&] {
+        if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "node solve: p must be >= 1"};
+        CtxLock lk(ctx);
+        // factor one node, solve with a complex RHS: W = S^{-1} (Br + i Bi)
+        // = S^{-1} Br + i S^{-1} Bi, each through the real-RHS path
+        const int n = A->n, N = A->N;
+        fl_filter f;
+        f.ctx = ctx;
+        f.A = A;
+        f.nc = 1;
+        f.zr = {zr};
+        f.zi = {zi};
+        f.wr = {1.0};
+        f.wi = {0.0};
+        f.cache = true;
+        f.kb = 0;
+        f.ke = 1;
+        f.factored.assign(1, 0);
+        const int P = round_up(2 * p, FL_TILE);
+        DBuf X;
+        X.ensure(sizeof(double) * (size_t)N * P);
+        CK(cudaMemsetAsync(X.p, 0, sizeof(double) * (size_t)N * P, ctx->stream));
+        std::vector<double> h((size_t)n * 2 * p);
+        for (int c = 0; c < p; ++c)
+            for (int i = 0; i < n; ++i) {
+                h[(size_t)c * n + i] = B[2 * ((size_t)c * n + i)];
+                h[(size_t)(p + c) * n + i] = B[2 * ((size_t)c * n + i) + 1];
+            }
+        copy_in(ctx, X.d(), N, n, h.data(), n, 2 * p, FL_HOST);
+        DBuf Y;
+        Y.ensure(sizeof(double) * (size_t)N * P);
+        // weight 1: Y = Re(W) for the real RHS; fetch W planes directly
+        filter_apply_dev(&f, X.d(), N, 2 * p, Y.d(), N, nullptr, nullptr);
+        std::vector<double> wr((size_t)N * P), wi((size_t)N * P);
+        CK(cudaMemcpyAsync(wr.data(), f.w_re.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(wi.data(), f.w_im.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        sync(ctx);
+        for (int c = 0; c < p; ++c)
+            for (int i = 0; i < n; ++i) {
+                // (S^{-1} Br) + i (S^{-1} Bi)
+                const double ar = wr[(size_t)c * N + i], ai = wi[(size_t)c * N + i];
+                const double br = wr[(size_t)(p + c) * N + i], bi = wi[(size_t)(p + c) * N + i];
+                W[2 * ((size_t)c * n + i)] = ar - bi;
+                W[2 * ((size_t)c * n + i) + 1] = ai + br;
+            }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// DMMA GEMM kernels (sm_100a): real C = alpha op(A) op(B) + beta C, and the
+// planar-complex update C -= A B used by the LU trailing update and the
+// blocked triangular solves of the filter.
+#include "gemm.cuh"
+#include "kernels.hpp"
+
+namespace fl {
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) dgemm_kernel(DGemm g) {
+    constexpr bool AKC = TA, BKC = !TB;
+    constexpr int S = 3;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;                       // S tiles
+    double* Bs = smem + S * TILE_DOUBLES;    // S tiles
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
+    const long z = blockIdx.z;
+    const double* A = g.A + z * g.strideA;
+    const double* B = g.B + z * g.strideB;
+    double* C = g.C + z * g.strideC;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int KT = g.K / GK;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+        if (s < KT) {
+            load_tile<AKC>(As + s * TILE_DOUBLES, tile_ptr<AKC>(A, g.lda, m0, s * GK), g.lda, tid);
+            load_tile<BKC>(Bs + s * TILE_DOUBLES, tile_ptr<BKC>(B, g.ldb, n0, s * GK), g.ldb, tid);
+        }
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<S - 2>();
+        __syncthreads();
+        const int nk = kt + S - 1;
+        if (nk < KT) {
+            const int st = nk % S;
+            load_tile<AKC>(As + st * TILE_DOUBLES, tile_ptr<AKC>(A, g.lda, m0, nk * GK), g.lda, tid);
+            load_tile<BKC>(Bs + st * TILE_DOUBLES, tile_ptr<BKC>(B, g.ldb, n0, nk * GK), g.ldb, tid);
+        }
+        cp_async_commit();
+        const double* as = As + (kt % S) * TILE_DOUBLES;
+        const double* bs = Bs + (kt % S) * TILE_DOUBLES;
+#pragma unroll
+        for (int kk = 0; kk < GK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = frag<AKC>(as, wm + i * 8 + gq, kk + tq);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = frag<BKC>(bs, wn + j * 8 + gq, kk + tq);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+    // epilogue
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm + i * 8 + gq;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = n0 + wn + j * 8 + 2 * tq + e;
+                double* cp = C + (long)col * g.ldc + row;
+                double v = g.alpha * acc[i][j][e];
+                if (g.beta != 0.0) v += g.beta * *cp;
+                *cp = v;
+            }
+        }
+    }
+}
+
+// C -= A * B (planar complex). A: MxK "MK", B: KxN "KM".
+__global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
+    extern __shared__ __align__(16) double smem[];
+    // per stage: Ar, Ai, Br, Bi
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
+    const long z = blockIdx.z;
+    const double* Ar = g.Ar + z * g.strideA;
+    const double* Ai = g.Ai + z * g.strideA;
+    const double* Br = g.Br + z * g.strideB;
+    const double* Bi = g.Bi + z * g.strideB;
+    double* Cr = g.Cr + z * g.strideC;
+    double* Ci = g.Ci + z * g.strideC;
+
+    double accr[4][4][2], acci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+
+    auto issue = [&](int st, int kt) {
+        double* base = smem + st * 4 * TILE_DOUBLES;
+        load_tile<false>(base, tile_ptr<false>(Ar, g.lda, m0, kt * GK), g.lda, tid);
+        load_tile<false>(base + TILE_DOUBLES, tile_ptr<false>(Ai, g.lda, m0, kt * GK), g.lda, tid);
+        load_tile<true>(base + 2 * TILE_DOUBLES, tile_ptr<true>(Br, g.ldb, n0, kt * GK), g.ldb, tid);
+        load_tile<true>(base + 3 * TILE_DOUBLES, tile_ptr<true>(Bi, g.ldb, n0, kt * GK), g.ldb, tid);
+    };
+
+    const int KT = g.K / GK;
+    issue(0, 0);
+    cp_async_commit();
+    for (int kt = 0; kt < KT; ++kt) {
+        cp_async_wait<0>();
+        __syncthreads();
+        if (kt + 1 < KT) issue((kt + 1) & 1, kt + 1);
+        cp_async_commit();
+        const double* base = smem + (kt & 1) * 4 * TILE_DOUBLES;
+        const double* ar_s = base;
+        const double* ai_s = base + TILE_DOUBLES;
+        const double* br_s = base + 2 * TILE_DOUBLES;
+        const double* bi_s = base + 3 * TILE_DOUBLES;
+#pragma unroll
+        for (int kk = 0; kk < GK; kk += 4) {
+            double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                ar[i] = frag<false>(ar_s, wm + i * 8 + gq, kk + tq);
+                ai[i] = frag<false>(ai_s, wm + i * 8 + gq, kk + tq);
+                nai[i] = -ai[i];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                br[j] = frag<true>(br_s, wn + j * 8 + gq, kk + tq);
+                bi[j] = frag<true>(bi_s, wn + j * 8 + gq, kk + tq);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    dmma(accr[i][j], ar[i], br[j]);
+                    dmma(acci[i][j], ar[i], bi[j]);
+                    dmma(accr[i][j], nai[i], bi[j]);
+                    dmma(acci[i][j], ai[i], br[j]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm + i * 8 + gq;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long off = (long)(n0 + wn + j * 8 + 2 * tq + e) * g.ldc + row;
+                Cr[off] -= accr[i][j][e];
+                Ci[off] -= acci[i][j][e];
+            }
+        }
+    }
+}
+
+void launch_dgemm(const DGemm& g, bool ta, bool tb, int batch, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0 || batch <= 0) return;
+    dim3 grid(g.M / GB, g.N / GB, batch);
+    const size_t sm = 3 * 2 * TILE_DOUBLES * sizeof(double);
+#define FL_DG(TA, TB)                                                                        \
+    {                                                                                        \
+        ensure_smem((const void*)dgemm_kernel<TA, TB>, sm);                                  \
+        dgemm_kernel<TA, TB><<<grid, 128, sm, s>>>(g);                                       \
+    }
+    if (!ta && !tb) FL_DG(false, false)
+    else if (ta && !tb) FL_DG(true, false)
+    else if (!ta && tb) FL_DG(false, true)
+    else FL_DG(true, true)
+#undef FL_DG
+}
+
+void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0 || batch <= 0) return;
+    dim3 grid(g.M / GB, g.N / GB, batch);
+    const size_t sm = 2 * 4 * TILE_DOUBLES * sizeof(double);
+    ensure_smem((const void*)zgemm_sub_kernel, sm);
+    zgemm_sub_kernel<<<grid, 128, sm, s>>>(g);
+}
+
+}  // namespace fl

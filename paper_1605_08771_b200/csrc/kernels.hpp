@@ -1,0 +1,69 @@
+// Internal launch interface of the sm_100a kernels (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fl {
+
+// Opt a kernel into > 48 KB dynamic shared memory once per (kernel, device).
+void ensure_smem(const void* func, size_t bytes);
+
+// Real C = alpha op(A) op(B) + beta C. M, N multiples of 64; K multiple of 16.
+struct DGemm {
+    int M, N, K;
+    const double* A; long lda; long strideA;
+    const double* B; long ldb; long strideB;
+    double* C; long ldc; long strideC;
+    double alpha, beta;
+};
+void launch_dgemm(const DGemm& g, bool ta, bool tb, int batch, cudaStream_t s);
+
+// Planar complex C -= A B. M, N multiples of 64; K multiple of 16.
+struct ZGemm {
+    int M, N, K;
+    const double *Ar, *Ai; long lda; long strideA;
+    const double *Br, *Bi; long ldb; long strideB;
+    double *Cr, *Ci; long ldc; long strideC;
+};
+void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s);
+
+// A planar-complex batch of N x N factor matrices: node b's planes start at
+// re + b*stride and im + b*stride, leading dimension ld (= N).
+struct ZBatch {
+    double* re;
+    double* im;
+    long ld;
+    long stride;
+};
+
+constexpr int kMaxNodes = 64;
+struct NodeShifts {
+    double zr[kMaxNodes];
+    double zi[kMaxNodes];
+};
+
+// F_b = z_b I - A (A real N x N, zero-padded beyond n).
+void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& z, int batch,
+                  cudaStream_t s);
+// Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j].
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int batch, cudaStream_t s);
+// Apply the panel's 64 row interchanges to all columns outside the panel.
+void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cudaStream_t s);
+// B <- L^{-1} B for the unit-lower 64x64 block at (k0, k0); B = F[k0:k0+64, c0:c0+ncols].
+void launch_trsm_unit_lower(ZBatch L, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
+                            cudaStream_t s);
+// B <- U^{-1} B for the upper 64x64 block at (k0, k0).
+void launch_trsm_upper(ZBatch U, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
+                       cudaStream_t s);
+// perm[b*N + i] from the row interchanges ipiv (LAPACK-style sequence).
+void launch_ipiv_to_perm(const int* ipiv, int* perm, int N, int batch, cudaStream_t s);
+// W_b = complex(P_b X): Wr[i,c] = X[perm[i], c], Wi = 0 for c < P.
+void launch_permute_rhs(const double* X, long ldx, int N, int P, const int* perm, ZBatch W,
+                        int batch, cudaStream_t s);
+// Y (+)= sum_{b ascending} Re(w_b W_b): Y = beta*Y + sum (beta in {0,1}).
+void launch_accumulate(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* Y, long ldy,
+                       bool add_to_Y, cudaStream_t s);
+// |U_ii| > 0 and finite for all i < n; on failure atomicMin(bad_node, offset + b).
+void launch_check_diag(ZBatch F, int n, int batch, int offset, int* bad_node, cudaStream_t s);
+
+}  // namespace fl

@@ -1,0 +1,456 @@
+// Complex partial-pivot LU of z I - A and the blocked multi-RHS solve
+// (NodeFactorization, proj/src/filterop.cpp:9-32), batched over contour nodes.
+//
+//  shift        F = z I - A                          HBM stream, 24 N^2 B / node
+//  panel        64-wide panel, partial pivoting      8-CTA cluster, DSMEM pivot
+//                                                    exchange, 1 cluster barrier / column
+//  laswp        row interchanges outside the panel
+//  trsm         64x64 triangular blocks (unit-lower / upper) on a column strip
+//  zgemm_sub    trailing update / solve updates      DMMA (gemm.cu)
+#include <cooperative_groups.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace fl {
+
+void ensure_smem(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({func, dev}).second)
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// ------------------------------------------------------------------ shift
+__global__ void shift_kernel(const double* __restrict__ A, long lda, int N, ZBatch F,
+                             NodeShifts z) {
+    const int b = blockIdx.y;
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    const long total = (long)N * N;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e / N, r = e - c * N;
+        double a = -A[c * lda + r];
+        double im = 0.0;
+        if (r == c) {
+            a += z.zr[b];
+            im = z.zi[b];
+        }
+        Fr[c * F.ld + r] = a;
+        Fi[c * F.ld + r] = im;
+    }
+}
+
+void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& z, int batch,
+                  cudaStream_t s) {
+    int blocks = 148 * 4 / (batch > 0 ? batch : 1);
+    if (blocks < 8) blocks = 8;
+    shift_kernel<<<dim3(blocks, batch), 256, 0, s>>>(A, lda, N, F, z);
+}
+
+// ------------------------------------------------------------------ panel
+// Cluster of PCL CTAs per node. CTA r owns panel rows [k0 + r*R, k0 + (r+1)*R).
+// Per column j (one cluster barrier):
+//   every CTA published (score, row) of its best candidate for column j plus a
+//   copy of that candidate row's 64 panel entries, and the owner of row j a
+//   copy of row j (double-buffered by j parity) -> after the barrier each CTA
+//   reduces the PCL candidates (ties -> lowest row, Eigen's maxCoeff), takes the
+//   pivot row from the winner's shared memory (DSMEM) and the owners of rows j
+//   and piv write the interchanged rows; then each CTA scales its rows of
+//   column j and applies the rank-1 update to the panel columns right of j,
+//   fusing the candidate search for column j+1.
+constexpr int PCL = 8;
+constexpr int PTH = 512;
+constexpr int PW = 64;
+
+struct PanelShared {
+    double cand_score[2];
+    int cand_row[2];
+    double cand_vals[2][2][PW];  // [parity][re/im][col]
+    double diag_vals[2][2][PW];
+    double u[2][PW];             // pivot row (this column)
+    double red_s[PTH / 32];
+    int red_i[PTH / 32];
+    int piv;
+    int winner;
+};
+
+__global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
+    panel_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv) {
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ PanelShared sh;
+    const int rank = (int)cluster.block_rank();
+    const int b = blockIdx.y;
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    const long ld = F.ld;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int rows_total = N - k0;
+    const int R = (rows_total + PCL - 1) / PCL;
+    const int lo = k0 + rank * R;
+    const int hi = min(N, lo + R);
+
+    auto at = [&](int r, int c) { return (long)c * ld + r; };
+
+    // candidate search for column c over own rows >= rmin, then publish
+    auto publish = [&](int c, int par, double s, int idx) {
+        warp_argmax(s, idx);
+        if (lane == 0) { sh.red_s[wid] = s; sh.red_i[wid] = idx; }
+        __syncthreads();
+        if (wid == 0) {
+            double s2 = lane < PTH / 32 ? sh.red_s[lane] : -1.0;
+            int i2 = lane < PTH / 32 ? sh.red_i[lane] : 0x7fffffff;
+            warp_argmax(s2, i2);
+            if (lane == 0) { sh.cand_score[par] = s2; sh.cand_row[par] = i2; }
+        }
+        __syncthreads();
+        const int cr = sh.cand_row[par];
+        if (tid < PW) {
+            if (cr >= 0 && cr < N) {
+                sh.cand_vals[par][0][tid] = Fr[at(cr, k0 + tid)];
+                sh.cand_vals[par][1][tid] = Fi[at(cr, k0 + tid)];
+            }
+            if (c >= lo && c < hi) {
+                sh.diag_vals[par][0][tid] = Fr[at(c, k0 + tid)];
+                sh.diag_vals[par][1][tid] = Fi[at(c, k0 + tid)];
+            }
+        }
+    };
+
+    // initial candidates for column k0
+    {
+        double s = -1.0;
+        int idx = 0x7fffffff;
+        for (int r = max(lo, k0) + tid; r < hi; r += PTH) {
+            double re = Fr[at(r, k0)], im = Fi[at(r, k0)];
+            double sc = re * re + im * im;
+            if (better(sc, r, s, idx)) { s = sc; idx = r; }
+        }
+        if (lo >= hi) idx = -1;
+        publish(k0, 0, s, idx);
+    }
+
+    for (int jj = 0; jj < PW; ++jj) {
+        const int j = k0 + jj;
+        const int par = jj & 1;
+        cluster.sync();
+        if (wid == 0) {
+            double s = -1.0;
+            int idx = 0x7fffffff, win = 0;
+            if (lane < PCL) {
+                PanelShared* rs = cluster.map_shared_rank(&sh, lane);
+                s = rs->cand_score[par];
+                idx = rs->cand_row[par];
+                if (idx < 0) { s = -1.0; idx = 0x7fffffff; }
+            }
+            int myrank = lane;
+            // argmax carrying the owning rank
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                double so = __shfl_xor_sync(0xffffffffu, s, off);
+                int io = __shfl_xor_sync(0xffffffffu, idx, off);
+                int ro = __shfl_xor_sync(0xffffffffu, myrank, off);
+                if (better(so, io, s, idx)) { s = so; idx = io; myrank = ro; }
+            }
+            win = myrank;
+            if (lane == 0) {
+                // all-zero column: Eigen keeps the diagonal row (no interchange)
+                if (!(s > 0.0)) idx = j;
+                sh.piv = idx;
+                sh.winner = win;
+            }
+        }
+        __syncthreads();
+        const int piv = sh.piv;
+        const int diag_owner = (j - k0) / R;
+        if (tid < PW) {
+            double ur, ui;
+            if (piv == j) {
+                PanelShared* ds = cluster.map_shared_rank(&sh, diag_owner);
+                ur = ds->diag_vals[par][0][tid];
+                ui = ds->diag_vals[par][1][tid];
+            } else {
+                PanelShared* ws = cluster.map_shared_rank(&sh, sh.winner);
+                ur = ws->cand_vals[par][0][tid];
+                ui = ws->cand_vals[par][1][tid];
+                if (piv >= lo && piv < hi) {
+                    // row piv receives the old row j
+                    PanelShared* ds = cluster.map_shared_rank(&sh, diag_owner);
+                    Fr[at(piv, k0 + tid)] = ds->diag_vals[par][0][tid];
+                    Fi[at(piv, k0 + tid)] = ds->diag_vals[par][1][tid];
+                }
+                if (j >= lo && j < hi) {
+                    Fr[at(j, k0 + tid)] = ur;
+                    Fi[at(j, k0 + tid)] = ui;
+                }
+            }
+            sh.u[0][tid] = ur;
+            sh.u[1][tid] = ui;
+        }
+        if (rank == 0 && tid == 0) ipiv[(long)b * N + j] = piv;
+        __syncthreads();
+        // scale column j, rank-1 update of columns j+1..k0+63, candidates for j+1
+        const cplx pv{sh.u[0][jj], sh.u[1][jj]};
+        const bool nonzero = (pv.re != 0.0 || pv.im != 0.0);
+        const cplx inv = nonzero ? crecip(pv) : cplx{0.0, 0.0};
+        double s = -1.0;
+        int idx = 0x7fffffff;
+        for (int r = max(lo, j + 1) + tid; r < hi; r += PTH) {
+            cplx l{Fr[at(r, j)], Fi[at(r, j)]};
+            if (nonzero) {
+                l = cmul(l, inv);
+                Fr[at(r, j)] = l.re;
+                Fi[at(r, j)] = l.im;
+            }
+            for (int c = jj + 1; c < PW; ++c) {
+                const long o = at(r, k0 + c);
+                const double ur = sh.u[0][c], ui = sh.u[1][c];
+                double xr = Fr[o], xi = Fi[o];
+                xr -= l.re * ur - l.im * ui;
+                xi -= l.re * ui + l.im * ur;
+                Fr[o] = xr;
+                Fi[o] = xi;
+                if (c == jj + 1) {
+                    double sc = xr * xr + xi * xi;
+                    if (better(sc, r, s, idx)) { s = sc; idx = r; }
+                }
+            }
+        }
+        if (jj + 1 < PW) {
+            if (max(lo, j + 1) >= hi) idx = -1;
+            __syncthreads();
+            publish(j + 1, par ^ 1, s, idx);
+        }
+    }
+    cluster.sync();  // keep shared memory alive until every CTA is done reading it
+}
+
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int batch, cudaStream_t s) {
+    panel_kernel<<<dim3(PCL, batch), PTH, 0, s>>>(F, N, k0, ipiv);
+}
+
+// ------------------------------------------------------------------ laswp
+// One thread per column outside the panel; the 64 interchanges in order.
+__global__ void laswp_panel_kernel(ZBatch F, int N, int k0, const int* __restrict__ ipiv) {
+    const int b = blockIdx.y;
+    int col = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ncols = N - PW;
+    if (col >= ncols) return;
+    if (col >= k0) col += PW;
+    double* Fr = F.re + b * F.stride + (long)col * F.ld;
+    double* Fi = F.im + b * F.stride + (long)col * F.ld;
+    const int* ip = ipiv + (long)b * N;
+    for (int j = k0; j < k0 + PW; ++j) {
+        const int p = ip[j];
+        if (p != j) {
+            double tr = Fr[j], ti = Fi[j];
+            Fr[j] = Fr[p];
+            Fi[j] = Fi[p];
+            Fr[p] = tr;
+            Fi[p] = ti;
+        }
+    }
+}
+
+void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cudaStream_t s) {
+    const int ncols = N - PW;
+    if (ncols <= 0) return;
+    laswp_panel_kernel<<<dim3((ncols + 127) / 128, batch), 128, 0, s>>>(F, N, k0, ipiv);
+}
+
+// ------------------------------------------------------------------ triangular 64x64 blocks
+// Strip of 32 RHS columns per CTA, 256 threads: thread (col = tid&31, q = tid>>5)
+// owns rows q, q+8, ..., q+56 of its column, in shared memory.
+constexpr int TS_COLS = 32;
+struct TriShared {
+    double Lr[PW][PW + 1];
+    double Li[PW][PW + 1];
+    double Xr[PW][TS_COLS + 1];
+    double Xi[PW][TS_COLS + 1];
+};
+
+template <bool UPPER>
+__global__ void __launch_bounds__(256) trsm64_kernel(ZBatch T, int k0, ZBatch B, int brow0,
+                                                     int bcol0, int ncols) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    TriShared& sh = *reinterpret_cast<TriShared*>(raw);
+    const int b = blockIdx.y;
+    const double* Tr = T.re + b * T.stride;
+    const double* Ti = T.im + b * T.stride;
+    double* Br = B.re + b * B.stride;
+    double* Bi = B.im + b * B.stride;
+    const int tid = threadIdx.x;
+    const int c0 = blockIdx.x * TS_COLS;
+    // load the triangle (row i, col k) and the RHS strip
+    for (int e = tid; e < PW * PW; e += 256) {
+        const int i = e & (PW - 1), k = e >> 6;
+        const long o = (long)(k0 + k) * T.ld + k0 + i;
+        sh.Lr[i][k] = Tr[o];
+        sh.Li[i][k] = Ti[o];
+    }
+    for (int e = tid; e < PW * TS_COLS; e += 256) {
+        const int i = e & (PW - 1), c = e >> 6;
+        if (c0 + c < ncols) {
+            const long o = (long)(bcol0 + c0 + c) * B.ld + brow0 + i;
+            sh.Xr[i][c] = Br[o];
+            sh.Xi[i][c] = Bi[o];
+        } else {
+            sh.Xr[i][c] = 0.0;
+            sh.Xi[i][c] = 0.0;
+        }
+    }
+    __syncthreads();
+    const int col = tid & 31, q = tid >> 5;
+    if (!UPPER) {
+        for (int r = 0; r < PW - 1; ++r) {
+            const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
+            for (int i = q; i < PW; i += 8) {
+                if (i > r) {
+                    const cplx l{sh.Lr[i][r], sh.Li[i][r]};
+                    sh.Xr[i][col] -= l.re * x.re - l.im * x.im;
+                    sh.Xi[i][col] -= l.re * x.im + l.im * x.re;
+                }
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int r = PW - 1; r >= 0; --r) {
+            if (q == (r & 7)) {
+                const cplx d{sh.Lr[r][r], sh.Li[r][r]};
+                const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
+                // x / d (complex division as std::complex does: x * conj(d) / |d|^2 scaled)
+                const cplx inv = crecip(d);
+                const cplx y = cmul(x, inv);
+                sh.Xr[r][col] = y.re;
+                sh.Xi[r][col] = y.im;
+            }
+            __syncthreads();
+            const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
+            for (int i = q; i < r; i += 8) {
+                const cplx u{sh.Lr[i][r], sh.Li[i][r]};
+                sh.Xr[i][col] -= u.re * x.re - u.im * x.im;
+                sh.Xi[i][col] -= u.re * x.im + u.im * x.re;
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < PW * TS_COLS; e += 256) {
+        const int i = e & (PW - 1), c = e >> 6;
+        if (c0 + c < ncols) {
+            const long o = (long)(bcol0 + c0 + c) * B.ld + brow0 + i;
+            Br[o] = sh.Xr[i][c];
+            Bi[o] = sh.Xi[i][c];
+        }
+    }
+}
+
+void launch_trsm_unit_lower(ZBatch L, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
+                            cudaStream_t s) {
+    if (ncols <= 0) return;
+    const size_t sm = sizeof(TriShared);
+    ensure_smem((const void*)trsm64_kernel<false>, sm);
+    trsm64_kernel<false><<<dim3((ncols + TS_COLS - 1) / TS_COLS, batch), 256, sm, s>>>(
+        L, k0, B, brow0, bcol0, ncols);
+}
+
+void launch_trsm_upper(ZBatch U, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
+                       cudaStream_t s) {
+    if (ncols <= 0) return;
+    const size_t sm = sizeof(TriShared);
+    ensure_smem((const void*)trsm64_kernel<true>, sm);
+    trsm64_kernel<true><<<dim3((ncols + TS_COLS - 1) / TS_COLS, batch), 256, sm, s>>>(
+        U, k0, B, brow0, bcol0, ncols);
+}
+
+// ------------------------------------------------------------------ pivots -> permutation
+__global__ void ipiv_to_perm_kernel(const int* __restrict__ ipiv, int* __restrict__ perm, int N) {
+    const int b = blockIdx.x;
+    const int* ip = ipiv + (long)b * N;
+    int* pm = perm + (long)b * N;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < N; ++i) pm[i] = i;
+        for (int i = 0; i < N; ++i) {
+            const int p = ip[i];
+            if (p != i) {
+                int t = pm[i];
+                pm[i] = pm[p];
+                pm[p] = t;
+            }
+        }
+    }
+}
+
+void launch_ipiv_to_perm(const int* ipiv, int* perm, int N, int batch, cudaStream_t s) {
+    ipiv_to_perm_kernel<<<batch, 32, 0, s>>>(ipiv, perm, N);
+}
+
+__global__ void permute_rhs_kernel(const double* __restrict__ X, long ldx, int N, int P,
+                                   const int* __restrict__ perm, ZBatch W) {
+    const int b = blockIdx.z;
+    const int c = blockIdx.y;
+    const int* pm = perm + (long)b * N;
+    double* Wr = W.re + b * W.stride + (long)c * W.ld;
+    double* Wi = W.im + b * W.stride + (long)c * W.ld;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        Wr[i] = X[(long)c * ldx + pm[i]];
+        Wi[i] = 0.0;
+    }
+}
+
+void launch_permute_rhs(const double* X, long ldx, int N, int P, const int* perm, ZBatch W,
+                        int batch, cudaStream_t s) {
+    if (P <= 0) return;
+    permute_rhs_kernel<<<dim3((N + 255) / 256, P, batch), 256, 0, s>>>(X, ldx, N, P, perm, W);
+}
+
+// ------------------------------------------------------------------ ordered accumulation
+// Y = [Y +] sum_b Re(w_b W_b), b ascending; Re(w W) = wr*Wr - wi*Wi with the
+// two products and the difference each rounded (std::complex product, no FMA),
+// exactly as proj/src/filterop.cpp:80 evaluates it.
+__global__ void accumulate_kernel(ZBatch W, int N, int P, NodeShifts w, int batch, double* Y,
+                                  long ldy, bool add) {
+    const long total = (long)N * P;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e / N, r = e - c * N;
+        double y = add ? Y[c * ldy + r] : 0.0;
+        for (int b = 0; b < batch; ++b) {
+            const long o = b * W.stride + c * W.ld + r;
+            const double t = __dsub_rn(__dmul_rn(w.zr[b], W.re[o]), __dmul_rn(w.zi[b], W.im[o]));
+            y = __dadd_rn(y, t);
+        }
+        Y[c * ldy + r] = y;
+    }
+}
+
+void launch_accumulate(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* Y, long ldy,
+                       bool add_to_Y, cudaStream_t s) {
+    if (P <= 0) return;
+    accumulate_kernel<<<148 * 4, 256, 0, s>>>(W, N, P, w, batch, Y, ldy, add_to_Y);
+}
+
+// ------------------------------------------------------------------ singularity check
+__global__ void check_diag_kernel(ZBatch F, int n, int offset, int* bad_node) {
+    const int b = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long o = b * F.stride + (long)i * F.ld + i;
+        const double d = hypot(F.re[o], F.im[o]);
+        if (!(d > 0.0) || !isfinite(d)) atomicMin(bad_node, offset + b);
+    }
+}
+
+void launch_check_diag(ZBatch F, int n, int batch, int offset, int* bad_node, cudaStream_t s) {
+    check_diag_kernel<<<dim3((n + 255) / 256, batch), 256, 0, s>>>(F, n, offset, bad_node);
+}
+
+}  // namespace fl

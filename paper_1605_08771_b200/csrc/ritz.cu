@@ -1,0 +1,532 @@
+// Rayleigh-Ritz / orthonormalisation device kernels (proj/src/ritz.cpp:17-122):
+// symmetrise, blocked Cholesky with first-failing-pivot report, real 64x64
+// triangular blocks, parallel cyclic Jacobi symmetric eigensolver (ascending
+// output, SelfAdjointEigenSolver's order), column norms / scaling / residual /
+// gather streams.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "ritz_kernels.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace fl {
+
+// ------------------------------------------------------------------ streams
+__global__ void symmetrize_kernel(const double* __restrict__ M, long ldm, int p, double* S,
+                                  long lds) {
+    const long total = (long)p * p;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / p), i = (int)(e - (long)j * p);
+        S[(long)j * lds + i] = 0.5 * (M[(long)j * ldm + i] + M[(long)i * ldm + j]);
+    }
+}
+void launch_symmetrize(const double* M, long ldm, int p, double* S, long lds, cudaStream_t s) {
+    if (p <= 0) return;
+    symmetrize_kernel<<<148 * 2, 256, 0, s>>>(M, ldm, p, S, lds);
+}
+
+__global__ void set_diag_kernel(double* M, long ld, int from, int to, double v) {
+    int i = from + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < to) M[(long)i * ld + i] = v;
+}
+void launch_set_diag(double* M, long ld, int from, int to, double v, cudaStream_t s) {
+    if (to <= from) return;
+    set_diag_kernel<<<(to - from + 255) / 256, 256, 0, s>>>(M, ld, from, to, v);
+}
+
+// column 2-norms, fixed-shape tree reduction (run-to-run deterministic)
+__global__ void col_norms_kernel(const double* __restrict__ X, long ldx, int n, double* norms) {
+    const int c = blockIdx.x;
+    const double* x = X + (long)c * ldx;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
+    s = warp_sum(s);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        norms[c] = sqrt(t);
+    }
+}
+void launch_col_norms(const double* X, long ldx, int n, int p, double* norms, cudaStream_t s) {
+    if (p <= 0) return;
+    col_norms_kernel<<<p, 256, 0, s>>>(X, ldx, n, norms);
+}
+
+// X[:, j] /= d[j]
+__global__ void col_div_kernel(double* X, long ldx, int n, const double* __restrict__ d) {
+    const int c = blockIdx.y;
+    const double dv = d[c];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        X[(long)c * ldx + i] /= dv;
+}
+void launch_col_div(double* X, long ldx, int n, int p, const double* d, cudaStream_t s) {
+    if (p <= 0) return;
+    col_div_kernel<<<dim3((n + 255) / 256, p), 256, 0, s>>>(X, ldx, n, d);
+}
+
+// R = AV - V diag(lam)   (Eigen evaluates A*V into a temporary, then subtracts)
+__global__ void residual_kernel(const double* __restrict__ AV, long ldav, const double* __restrict__ V,
+                                long ldv, int n, const double* __restrict__ lam, double* R,
+                                long ldr) {
+    const int c = blockIdx.y;
+    const double l = lam[c];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        R[(long)c * ldr + i] = AV[(long)c * ldav + i] - V[(long)c * ldv + i] * l;
+}
+void launch_residual(const double* AV, long ldav, const double* V, long ldv, int n, int p,
+                     const double* lam, double* R, long ldr, cudaStream_t s) {
+    if (p <= 0) return;
+    residual_kernel<<<dim3((n + 255) / 256, p), 256, 0, s>>>(AV, ldav, V, ldv, n, lam, R, ldr);
+}
+
+// dst[:, j] = src[:, idx[j]] for j < k; columns k..kpad-1 of dst zeroed
+__global__ void gather_cols_kernel(const double* __restrict__ src, long lds, int n,
+                                   const int* __restrict__ idx, int k, double* dst, long ldd) {
+    const int c = blockIdx.y;
+    const double* s = c < k ? src + (long)idx[c] * lds : nullptr;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[(long)c * ldd + i] = s ? s[i] : 0.0;
+}
+void launch_gather_cols(const double* src, long lds, int n, const int* idx, int k, int kpad,
+                        double* dst, long ldd, cudaStream_t s) {
+    if (kpad <= 0) return;
+    gather_cols_kernel<<<dim3((n + 255) / 256, kpad), 256, 0, s>>>(src, lds, n, idx, k, dst, ldd);
+}
+
+// ------------------------------------------------------------------ Cholesky
+// Diagonal 64x64 block, in shared memory, the reference's column algorithm
+// (proj/src/ritz.cpp:64-79) on the already-updated block; reports the first
+// pivot s <= 0 or non-finite (global index kb + j) into info[0..1].
+struct CholInfo {
+    int index;   // -1 = ok
+    double pivot;
+};
+
+__global__ void __launch_bounds__(256) chol_diag_kernel(double* B, long ld, int kb, int limit,
+                                                        CholInfo* info) {
+    __shared__ double L[64][65];
+    __shared__ int fail;
+    const int tid = threadIdx.x;
+    if (info->index >= 0) return;  // an earlier block already failed
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int i = e & 63, k = e >> 6;
+        L[i][k] = B[(long)(kb + k) * ld + kb + i];
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < 64; ++j) {
+        if (tid == 0) {
+            double s = L[j][j];
+            for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+            if (kb + j < limit && (!(s > 0.0) || !isfinite(s))) {
+                info->index = kb + j;
+                info->pivot = s;
+                fail = 1;
+            }
+            L[j][j] = sqrt(s);
+        }
+        __syncthreads();
+        if (fail) return;
+        for (int i = j + 1 + tid; i < 64; i += 256) {
+            double t = L[i][j];
+            for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+            L[i][j] = t / L[j][j];
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int i = e & 63, k = e >> 6;
+        B[(long)(kb + k) * ld + kb + i] = (i >= k) ? L[i][k] : 0.0;
+    }
+}
+
+// rows i in [kb+64, P): L[i, kb:kb+64] = B[i, kb:kb+64] L_kk^{-T}
+__global__ void __launch_bounds__(128) chol_panel_kernel(double* B, long ld, int kb, int P,
+                                                         const CholInfo* info) {
+    __shared__ double L[64][65];
+    if (info->index >= 0) return;
+    for (int e = threadIdx.x; e < 64 * 64; e += 128) {
+        const int i = e & 63, k = e >> 6;
+        L[i][k] = B[(long)(kb + k) * ld + kb + i];
+    }
+    __syncthreads();
+    const int row = kb + 64 + blockIdx.x * 128 + threadIdx.x;
+    if (row >= P) return;
+    double x[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+        double t = B[(long)(kb + j) * ld + row];
+#pragma unroll
+        for (int k = 0; k < j; ++k) t -= x[k] * L[j][k];
+        x[j] = t / L[j][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 64; ++j) B[(long)(kb + j) * ld + row] = x[j];
+}
+
+void launch_cholesky(double* B, long ld, int p, int P, void* info_dev, cudaStream_t s) {
+    CholInfo* info = static_cast<CholInfo*>(info_dev);
+    for (int kb = 0; kb < P; kb += 64) {
+        chol_diag_kernel<<<1, 256, 0, s>>>(B, ld, kb, p, info);
+        const int rest = P - kb - 64;
+        if (rest > 0) {
+            chol_panel_kernel<<<(rest + 127) / 128, 128, 0, s>>>(B, ld, kb, P, info);
+            DGemm g{rest, rest, 64, B + (long)kb * ld + kb + 64, ld, 0,
+                    B + (long)kb * ld + kb + 64, ld, 0,
+                    B + (long)(kb + 64) * ld + kb + 64, ld, 0, -1.0, 1.0};
+            launch_dgemm(g, false, true, 1, s);
+        }
+    }
+}
+
+// zero the strict upper triangle (L from the in-place Cholesky)
+__global__ void tril_kernel(double* B, long ld, int P) {
+    const long total = (long)P * P;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / P), i = (int)(e - (long)j * P);
+        if (i < j) B[(long)j * ld + i] = 0.0;
+    }
+}
+void launch_tril(double* B, long ld, int P, cudaStream_t s) {
+    tril_kernel<<<148, 256, 0, s>>>(B, ld, P);
+}
+
+// ------------------------------------------------------------------ real triangular 64x64 blocks
+// X[r0:r0+64, :] <- T^{-1} X or T^{-T} X, T = L[k0:k0+64, k0:k0+64] lower non-unit.
+template <bool TRANS>
+__global__ void __launch_bounds__(128) dtrsm64_kernel(const double* L, long ldl, int k0, double* X,
+                                                      long ldx, int r0, int ncols) {
+    __shared__ double T[64][65];
+    __shared__ double S[64][17];
+    const int tid = threadIdx.x, c0 = blockIdx.x * 16;
+    for (int e = tid; e < 64 * 64; e += 128) {
+        const int i = e & 63, k = e >> 6;
+        T[i][k] = L[(long)(k0 + k) * ldl + k0 + i];
+    }
+    for (int e = tid; e < 64 * 16; e += 128) {
+        const int i = e & 63, c = e >> 6;
+        S[i][c] = (c0 + c < ncols) ? X[(long)(c0 + c) * ldx + r0 + i] : 0.0;
+    }
+    __syncthreads();
+    const int col = tid & 15, q = tid >> 4;
+    if (!TRANS) {  // forward: T lower
+        for (int r = 0; r < 64; ++r) {
+            if (q == (r & 7)) S[r][col] /= T[r][r];
+            __syncthreads();
+            const double x = S[r][col];
+            for (int i = q; i < 64; i += 8)
+                if (i > r) S[i][col] -= T[i][r] * x;
+            __syncthreads();
+        }
+    } else {  // backward with T^T (upper): (T^T)[i][r] = T[r][i]
+        for (int r = 63; r >= 0; --r) {
+            if (q == (r & 7)) S[r][col] /= T[r][r];
+            __syncthreads();
+            const double x = S[r][col];
+            for (int i = q; i < r; i += 8) S[i][col] -= T[r][i] * x;
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < 64 * 16; e += 128) {
+        const int i = e & 63, c = e >> 6;
+        if (c0 + c < ncols) X[(long)(c0 + c) * ldx + r0 + i] = S[i][c];
+    }
+}
+
+// X <- L^{-1} X (trans=false) or L^{-T} X (trans=true); L P x P lower with
+// identity padding, X P x ncols (ncols multiple of 64).
+void launch_trsm_lower(const double* L, long ldl, int P, double* X, long ldx, int ncols, bool trans,
+                       cudaStream_t s) {
+    const int NB = P / 64;
+    const int grid = (ncols + 15) / 16;
+    if (!trans) {
+        for (int ib = 0; ib < NB; ++ib) {
+            dtrsm64_kernel<false><<<grid, 128, 0, s>>>(L, ldl, ib * 64, X, ldx, ib * 64, ncols);
+            const int rest = P - (ib + 1) * 64;
+            if (rest > 0) {
+                DGemm g{rest, ncols, 64, L + (long)(ib * 64) * ldl + (ib + 1) * 64, ldl, 0,
+                        X + ib * 64, ldx, 0, X + (ib + 1) * 64, ldx, 0, -1.0, 1.0};
+                launch_dgemm(g, false, false, 1, s);
+            }
+        }
+    } else {
+        for (int ib = NB - 1; ib >= 0; --ib) {
+            dtrsm64_kernel<true><<<grid, 128, 0, s>>>(L, ldl, ib * 64, X, ldx, ib * 64, ncols);
+            const int above = ib * 64;
+            if (above > 0) {
+                // X[0:above] -= (L[ib*64:+64, 0:above])^T X[ib*64:+64]
+                DGemm g{above, ncols, 64, L + ib * 64, ldl, 0, X + ib * 64, ldx, 0, X, ldx, 0,
+                        -1.0, 1.0};
+                launch_dgemm(g, true, false, 1, s);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ Jacobi eigensolver
+// Parallel cyclic two-sided Jacobi with the round-robin (circle) ordering:
+// round r pairs (r, pe-1) and ((r+k) mod (pe-1), (r-k) mod (pe-1)), k >= 1.
+// Every CTA recomputes all rotations of the round from the current matrix
+// (double-buffered, so no intra-round hazards), then applies its share of the
+// 2x2 block updates A' = J^T A J and V' = V J: one grid barrier per round.
+// Rotations follow Golub & Van Loan sym.schur2; a pair is skipped when
+// |a_ab| <= thr = eps * ||A||_F. Converged when a sweep rotates nothing.
+struct JacobiArgs {
+    double* A0;
+    double* A1;
+    long lda;
+    double* V;
+    long ldv;
+    int p;       // true size
+    int pe;      // even size (p or p+1)
+    double thr;  // skip threshold
+    int max_sweeps;
+    int* sweeps_done;
+    unsigned long long* rot_count;  // per sweep counter, [max_sweeps]
+};
+
+__device__ __forceinline__ void round_pair(int r, int k, int pe, int& a, int& b) {
+    const int m = pe - 1;
+    if (k == 0) {
+        a = r;
+        b = m;
+    } else {
+        a = (r + k) % m;
+        b = (r - k + m) % m;
+    }
+    if (a > b) {
+        int t = a;
+        a = b;
+        b = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) jacobi_kernel(JacobiArgs J) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double jsh[];
+    const int half = J.pe / 2;
+    double* cs = jsh;              // [half]
+    double* sn = jsh + half;       // [half]
+    double* tt = jsh + 2 * half;   // [half] (t for the diagonal update)
+    int* pa = reinterpret_cast<int*>(jsh + 3 * half);  // [half]
+    int* pb = pa + half;                               // [half]
+    int* role = pb + half;                             // [pe]: pair index * 2 + (is_b)
+    __shared__ unsigned long long cnt;
+    const int p = J.p, pe = J.pe;
+    const long lda = J.lda;
+    double* Acur = J.A0;
+    double* Anext = J.A1;
+    auto el = [&](const double* M, int i, int j) -> double {
+        if (i >= p || j >= p) return 0.0;
+        return M[(long)j * lda + i];
+    };
+    int sweep = 0;
+    for (; sweep < J.max_sweeps; ++sweep) {
+        for (int r = 0; r < pe - 1; ++r) {
+            if (threadIdx.x == 0) cnt = 0;
+            __syncthreads();
+            // rotations of this round (every CTA, redundantly)
+            unsigned long long local = 0;
+            for (int k = threadIdx.x; k < half; k += blockDim.x) {
+                int a, b;
+                round_pair(r, k, pe, a, b);
+                pa[k] = a;
+                pb[k] = b;
+                role[a] = 2 * k;
+                role[b] = 2 * k + 1;
+                double c = 1.0, s = 0.0, t = 0.0;
+                if (b < p) {
+                    const double apq = el(Acur, a, b);
+                    if (fabs(apq) > J.thr) {
+                        const double app = el(Acur, a, a), aqq = el(Acur, b, b);
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        ++local;
+                    }
+                }
+                cs[k] = c;
+                sn[k] = s;
+                tt[k] = t;
+            }
+            if (local) atomicAdd(&cnt, local);
+            __syncthreads();
+            if (blockIdx.x == 0 && threadIdx.x == 0 && cnt) atomicAdd(&J.rot_count[sweep], cnt);
+            // apply: blocks (P, Q) of 2x2, all P, Q in [0, half)
+            const long nblk = (long)half * half;
+            for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nblk;
+                 e += (long)gridDim.x * blockDim.x) {
+                const int P = (int)(e % half), Q = (int)(e / half);
+                const int a1 = pa[P], b1 = pb[P], a2 = pa[Q], b2 = pb[Q];
+                const double c1 = cs[P], s1 = sn[P], c2 = cs[Q], s2 = sn[Q];
+                const double Baa = el(Acur, a1, a2), Bab = el(Acur, a1, b2);
+                const double Bba = el(Acur, b1, a2), Bbb = el(Acur, b1, b2);
+                double naa, nab, nba, nbb;
+                if (P == Q && s1 != 0.0) {
+                    const double t = tt[P];
+                    naa = Baa - t * Bab;
+                    nbb = Bbb + t * Bab;
+                    nab = 0.0;
+                    nba = 0.0;
+                } else {
+                    // rows: x_a = c1*row_a - s1*row_b ; x_b = s1*row_a + c1*row_b
+                    const double ra_a = c1 * Baa - s1 * Bba, ra_b = c1 * Bab - s1 * Bbb;
+                    const double rb_a = s1 * Baa + c1 * Bba, rb_b = s1 * Bab + c1 * Bbb;
+                    naa = ra_a * c2 - ra_b * s2;
+                    nab = ra_a * s2 + ra_b * c2;
+                    nba = rb_a * c2 - rb_b * s2;
+                    nbb = rb_a * s2 + rb_b * c2;
+                }
+                if (a1 < p && a2 < p) Anext[(long)a2 * lda + a1] = naa;
+                if (a1 < p && b2 < p) Anext[(long)b2 * lda + a1] = nab;
+                if (b1 < p && a2 < p) Anext[(long)a2 * lda + b1] = nba;
+                if (b1 < p && b2 < p) Anext[(long)b2 * lda + b1] = nbb;
+            }
+            // V' = V J on column pairs
+            const long nv = (long)p * half;
+            for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nv;
+                 e += (long)gridDim.x * blockDim.x) {
+                const int x = (int)(e % p), P = (int)(e / p);
+                const double s1 = sn[P];
+                if (s1 == 0.0) continue;
+                const int a = pa[P], b = pb[P];
+                if (b >= p) continue;
+                const double c1 = cs[P];
+                const double va = J.V[(long)a * J.ldv + x], vb = J.V[(long)b * J.ldv + x];
+                J.V[(long)a * J.ldv + x] = c1 * va - s1 * vb;
+                J.V[(long)b * J.ldv + x] = s1 * va + c1 * vb;
+            }
+            grid.sync();
+            double* t = Acur;
+            Acur = Anext;
+            Anext = t;
+        }
+        // all CTAs see the same counter after the last barrier of the sweep
+        const unsigned long long total = *(volatile unsigned long long*)&J.rot_count[sweep];
+        if (total == 0) {
+            ++sweep;
+            break;
+        }
+    }
+    // leave the final matrix in A0
+    if (Acur != J.A0) {
+        const long total = (long)p * p;
+        for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+             e += (long)gridDim.x * blockDim.x) {
+            const int j = (int)(e / p), i = (int)(e - (long)j * p);
+            J.A0[(long)j * lda + i] = Acur[(long)j * lda + i];
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *J.sweeps_done = sweep;
+}
+
+// ascending sort of the diagonal with its eigenvector columns:
+// rank(i) = #{j : d_j < d_i or (d_j == d_i and j < i)}
+__global__ void eig_sort_kernel(const double* __restrict__ A, long lda, int p,
+                                const double* __restrict__ V, long ldv, double* vals,
+                                double* Vout, long ldo) {
+    const int i = blockIdx.x;
+    const double di = A[(long)i * lda + i];
+    __shared__ int rank_s;
+    int cnt = 0;
+    for (int j = threadIdx.x; j < p; j += blockDim.x) {
+        const double dj = A[(long)j * lda + j];
+        cnt += (dj < di || (dj == di && j < i)) ? 1 : 0;
+    }
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    __shared__ int red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        rank_s = t;
+        vals[t] = di;
+    }
+    __syncthreads();
+    const int r = rank_s;
+    for (int x = threadIdx.x; x < p; x += blockDim.x) Vout[(long)r * ldo + x] = V[(long)i * ldv + x];
+}
+
+__global__ void eye_kernel(double* V, long ldv, int rows, int cols) {
+    const long total = (long)rows * cols;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / rows), i = (int)(e - (long)j * rows);
+        V[(long)j * ldv + i] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+__global__ void fro2_kernel(const double* A, long lda, int p, double* out) {
+    double s = 0.0;
+    const long total = (long)p * p;
+    for (long e = threadIdx.x; e < total; e += blockDim.x) {
+        const int j = (int)(e / p), i = (int)(e - (long)j * p);
+        const double v = A[(long)j * lda + i];
+        s += v * v;
+    }
+    s = warp_sum(s);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        *out = t;
+    }
+}
+
+void launch_fro2(const double* A, long lda, int p, double* out_dev, cudaStream_t s) {
+    fro2_kernel<<<1, 1024, 0, s>>>(A, lda, p, out_dev);
+}
+
+int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, long ldv,
+               double* vals, double* Vout, long ldo, int* scratch_int, unsigned long long* counters,
+               int max_sweeps, cudaStream_t s) {
+    if (p <= 0) return 0;
+    const int pe = p + (p & 1);
+    const int half = pe / 2;
+    eye_kernel<<<148, 256, 0, s>>>(V, ldv, p, p);
+    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * max_sweeps, s);
+    JacobiArgs J;
+    J.A0 = A;
+    J.A1 = work;
+    J.lda = lda;
+    J.V = V;
+    J.ldv = ldv;
+    J.p = p;
+    J.pe = pe;
+    J.thr = 2.220446049250313e-16 * fro;
+    if (!(J.thr > 0.0)) J.thr = 0.0;
+    J.max_sweeps = max_sweeps;
+    J.sweeps_done = scratch_int;
+    J.rot_count = counters;
+    const size_t sm = sizeof(double) * 3 * half + sizeof(int) * (2 * half + pe);
+    ensure_smem((const void*)jacobi_kernel, sm);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_kernel, 256, sm);
+    if (per_sm < 1) per_sm = 1;
+    int blocks = nsm * (per_sm > 2 ? 2 : per_sm);
+    const long work_items = (long)half * half;
+    if (work_items < (long)blocks * 256) {
+        blocks = (int)((work_items + 255) / 256);
+        if (blocks < 1) blocks = 1;
+    }
+    void* args[] = {&J};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(blocks), dim3(256),
+                                                args, sm, s);
+    if (e != cudaSuccess) return -1;
+    eig_sort_kernel<<<p, 256, 0, s>>>(A, lda, p, V, ldv, vals, Vout, ldo);
+    return 0;
+}
+
+}  // namespace fl

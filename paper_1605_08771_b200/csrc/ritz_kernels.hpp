@@ -1,0 +1,30 @@
+// Internal launch interface of the Rayleigh-Ritz kernels (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace fl {
+
+void launch_symmetrize(const double* M, long ldm, int p, double* S, long lds, cudaStream_t s);
+void launch_set_diag(double* M, long ld, int from, int to, double v, cudaStream_t s);
+void launch_col_norms(const double* X, long ldx, int n, int p, double* norms, cudaStream_t s);
+void launch_col_div(double* X, long ldx, int n, int p, const double* d, cudaStream_t s);
+void launch_residual(const double* AV, long ldav, const double* V, long ldv, int n, int p,
+                     const double* lam, double* R, long ldr, cudaStream_t s);
+void launch_gather_cols(const double* src, long lds, int n, const int* idx, int k, int kpad,
+                        double* dst, long ldd, cudaStream_t s);
+// In-place blocked Cholesky of the P x P matrix B (identity-padded beyond p);
+// info_dev -> {int index (-1 ok), double pivot}.
+void launch_cholesky(double* B, long ld, int p, int P, void* info_dev, cudaStream_t s);
+void launch_tril(double* B, long ld, int P, cudaStream_t s);
+void launch_trsm_lower(const double* L, long ldl, int P, double* X, long ldx, int ncols, bool trans,
+                       cudaStream_t s);
+void launch_fro2(const double* A, long lda, int p, double* out_dev, cudaStream_t s);
+// Symmetric eigensolve of the p x p matrix A (destroyed; work same shape):
+// ascending vals[p], eigenvectors Vout (ld ldo); V is scratch (ld ldv).
+int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, long ldv,
+               double* vals, double* Vout, long ldo, int* scratch_int, unsigned long long* counters,
+               int max_sweeps, cudaStream_t s);
+
+}  // namespace fl

@@ -18,3 +18,16 @@ def orc():
     import oracle
     oracle.lib()
     return oracle
+
+
+@pytest.fixture(params=["oracle", pytest.param("b200", marks=pytest.mark.gpu)])
+def F(request):
+    """The implementation under test: the CPU oracle (pins the restatement
+    against the reference's own assertions) or the B200 path."""
+    if request.param == "oracle":
+        import oracle
+        oracle.lib()
+        return oracle
+    import paper_1605_08771_b200 as P
+    P._lib.lib()
+    return P

@@ -1,5 +1,5 @@
-"""Oracle pin: re-expresses proj/tests/test_drivers.cpp, test_matmodel.cpp and
-acceptance C4/C5/C7/C8/C9/C10 (proj/tests/acceptance.cpp) against the oracle."""
+"""Re-expresses proj/tests/test_drivers.cpp, test_matmodel.cpp and
+acceptance C4/C5/C7/C8/C9/C10 (proj/tests/acceptance.cpp) against both the CPU oracle (pin) and the B200 path (F = b200, -m gpu)."""
 import numpy as np
 import pytest
 
@@ -51,17 +51,17 @@ def test_symmetric_matrix_check():  # matmodel.cpp:10-19
     assert S[0, 1] == S[1, 0]
 
 
-def test_initial_guess():  # test_drivers.cpp:22-29
-    a = O.make_initial_guess(4, 2, 7)
-    assert np.array_equal(a, O.make_initial_guess(4, 2, 7))
-    assert np.linalg.matrix_rank(O.make_initial_guess(4, 4, 3)) == 4
-    with pytest.raises(O.InvalidArgument):
-        O.make_initial_guess(4, 5, 1)
+def test_initial_guess(F):
+    a = F.make_initial_guess(4, 2, 7)
+    assert np.array_equal(a, F.make_initial_guess(4, 2, 7))
+    assert np.linalg.matrix_rank(F.make_initial_guess(4, 4, 3)) == 4
+    with pytest.raises(F.InvalidArgument):
+        F.make_initial_guess(4, 5, 1)
 
 
-def test_feast_4x4_diagonal():  # test_drivers.cpp:31-44
+def test_feast_4x4_diagonal(F):
     A = np.diag([-0.5, 0.5, 2.0, 3.0])
-    sol = O.feast_solve(A, I11, O.SolverConfig(m0=3, n_c=8, tol=1e-12))
+    sol = F.feast_solve(A, I11, F.SolverConfig(m0=3, n_c=8, tol=1e-12))
     assert sol.converged and sol.iterations <= 3
     assert len(sol.eigenvalues) == 2
     assert sol.eigenvalues[0] == pytest.approx(-0.5, rel=1e-12)
@@ -69,19 +69,19 @@ def test_feast_4x4_diagonal():  # test_drivers.cpp:31-44
     assert sol.residual_norms.max() <= 1e-12
 
 
-def test_xfeast_2x2():  # test_drivers.cpp:46-56
-    sol = O.xfeast_solve(np.diag([0.5, 2.0]), I11, O.SolverConfig(m0=1, s=2, n_c=8))
+def test_xfeast_2x2(F):
+    sol = F.xfeast_solve(np.diag([0.5, 2.0]), I11, F.SolverConfig(m0=1, s=2, n_c=8))
     assert sol.converged and len(sol.eigenvalues) == 1
     assert sol.eigenvalues[0] == pytest.approx(0.5, rel=1e-12)
 
 
 @pytest.mark.parametrize("seed", [11, 12])
 @pytest.mark.parametrize("driver", ["feast_solve", "xfeast_solve", "rfeast_solve"])
-def test_drivers_vs_dense_oracle(seed, driver):  # test_drivers.cpp:58-95
+def test_drivers_vs_dense_oracle(F, seed, driver):
     A = small_instance(seed)
     w, V = O.dense_eig(A)
     m_true = sum(1 for x in w if I11.contains(x))
-    sol = getattr(O, driver)(A, I11, O.SolverConfig(m0=8, n_c=8, s=2, tol=1e-10))
+    sol = getattr(O, driver)(A, I11, F.SolverConfig(m0=8, n_c=8, s=2, tol=1e-10))
     assert sol.converged and len(sol.eigenvalues) == m_true
     scale = np.linalg.norm(A)
     for k, lam in enumerate(sol.eigenvalues):
@@ -90,19 +90,19 @@ def test_drivers_vs_dense_oracle(seed, driver):  # test_drivers.cpp:58-95
         assert abs(V[:, j] @ sol.eigenvectors[:, k]) >= 1 - 1e-8
 
 
-def test_empty_interval():  # test_drivers.cpp:97-108
-    sol = O.feast_solve(np.diag([2.0, 3.0, 4.0, 5.0]), I11, O.SolverConfig(m0=2, n_c=4))
+def test_empty_interval(F):
+    sol = F.feast_solve(np.diag([2.0, 3.0, 4.0, 5.0]), I11, F.SolverConfig(m0=2, n_c=4))
     assert sol.converged and sol.iterations == 1 and len(sol.eigenvalues) == 0
     assert len(sol.trace) == 1 and sol.trace[0].m_found == 0
 
 
 @pytest.mark.parametrize("seed", [21, 22, 23])
-def test_s1_traces_match_feast(seed):  # test_drivers.cpp:110-135
+def test_s1_traces_match_feast(F, seed):
     A = small_instance(seed)
-    cfg = O.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=12)
-    f = O.feast_solve(A, I11, cfg)
-    x = O.xfeast_solve(A, I11, cfg)
-    r = O.rfeast_solve(A, I11, cfg)
+    cfg = F.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=12)
+    f = F.feast_solve(A, I11, cfg)
+    x = F.xfeast_solve(A, I11, cfg)
+    r = F.rfeast_solve(A, I11, cfg)
     assert len(x.trace) == len(f.trace) == len(r.trace)
     for tf, tx, tr in zip(f.trace, x.trace, r.trace):
         tol = 1e-6 * tf.max_residual + 1e-12
@@ -111,42 +111,42 @@ def test_s1_traces_match_feast(seed):  # test_drivers.cpp:110-135
         assert tx.rhs_cumulative == tf.rhs_cumulative == tr.rhs_cumulative
 
 
-def test_rhs_accounting_formula():  # test_drivers.cpp:137-160
+def test_rhs_accounting_formula(F):
     A = small_instance(31)
-    cfg = O.SolverConfig(m0=7, n_c=5, s=3, tol=1e-13, max_iter=6)
-    for rec in O.feast_solve(A, I11, cfg).trace:
+    cfg = F.SolverConfig(m0=7, n_c=5, s=3, tol=1e-13, max_iter=6)
+    for rec in F.feast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 7 * rec.iter
-    for rec in O.xfeast_solve(A, I11, cfg).trace:
+    for rec in F.xfeast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 7 * (rec.iter + max(cfg.s - 2, 0))
-    for rec in O.rfeast_solve(A, I11, cfg).trace:
+    for rec in F.rfeast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 7 * rec.iter
 
 
-def test_determinism_and_cache_invariance():  # test_drivers.cpp:162-196
+def test_determinism_and_cache_invariance(F):
     A = small_instance(41)
-    cfg = O.SolverConfig(m0=6, n_c=4, s=2, max_iter=8, tol=1e-13)
-    for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+    cfg = F.SolverConfig(m0=6, n_c=4, s=2, max_iter=8, tol=1e-13)
+    for d in (F.feast_solve, F.xfeast_solve, F.rfeast_solve):
         a, b = d(A, I11, cfg), d(A, I11, cfg)
         assert np.array_equal(a.eigenvalues, b.eigenvalues)
         assert np.array_equal(a.eigenvectors, b.eigenvectors)
         assert [t.max_residual for t in a.trace] == [t.max_residual for t in b.trace]
     A = small_instance(43)
-    cfg = O.SolverConfig(m0=6, n_c=4, max_iter=6, tol=1e-13)
-    plain = O.feast_solve(A, I11, cfg)
+    cfg = F.SolverConfig(m0=6, n_c=4, max_iter=6, tol=1e-13)
+    plain = F.feast_solve(A, I11, cfg)
     cfg.cache_factorizations = True
-    cached = O.feast_solve(A, I11, cfg)
+    cached = F.feast_solve(A, I11, cfg)
     assert np.array_equal(plain.eigenvalues, cached.eigenvalues)
     assert plain.accounting.rhs_solved == cached.accounting.rhs_solved
     assert cached.accounting.factorizations == 4
 
 
-def test_converged_run_ends_at_trace_minimum():  # test_drivers.cpp:198-208
-    sol = O.feast_solve(small_instance(47), I11, O.SolverConfig(m0=7, n_c=6, tol=1e-11))
+def test_converged_run_ends_at_trace_minimum(F):
+    sol = F.feast_solve(small_instance(47), I11, F.SolverConfig(m0=7, n_c=6, tol=1e-11))
     assert sol.converged
     assert all(sol.trace[-1].max_residual <= r.max_residual for r in sol.trace)
 
 
-def test_rate_prediction():  # test_drivers.cpp:210-243 and acceptance C8
+def test_rate_prediction(F):
     cases = [(32, 6, 2.5, 30.0, 61, 6, 6, 1e-14, 30, 42)]
     for k in range(5):
         n, m = 28 + 6 * k, 5 + k % 3
@@ -156,10 +156,10 @@ def test_rate_prediction():  # test_drivers.cpp:210-243 and acceptance C8
                                n - m, seed=lseed)
         vals, Q = O.generate_spectrum(lay)
         A = O.assemble_matrix(vals, Q)
-        rule = O.build_contour_rule(I11, nc)
+        rule = F.build_contour_rule(I11, nc)
         pred = O.predicted_rate(rule, vals, m0)
         assert pred <= 0.1
-        sol = O.feast_solve(A, I11, O.SolverConfig(m0=m0, n_c=nc, tol=tol, max_iter=mi, seed=xseed))
+        sol = F.feast_solve(A, I11, F.SolverConfig(m0=m0, n_c=nc, tol=tol, max_iter=mi, seed=xseed))
         prod, samples = 1.0, 0
         for a, b in zip(sol.trace[:-1], sol.trace[1:]):
             if a.max_residual < 1e-2 and a.max_residual > 1e-12 and b.max_residual > 1e-13:
@@ -170,20 +170,20 @@ def test_rate_prediction():  # test_drivers.cpp:210-243 and acceptance C8
             assert pred / 10 <= meas <= 10 * pred
 
 
-def test_trace_csv():  # test_drivers.cpp:245-252
-    assert O.write_trace_csv([O.TraceRecord(1, 8, 40, 0.125, 3)]) == (
+def test_trace_csv(F):
+    assert F.write_trace_csv([F.TraceRecord(1, 8, 40, 0.125, 3)]) == (
         "iter,subspace_dim,rhs_cumulative,max_residual,m_found\n1,8,40,0.125,3\n")
 
 
-def test_config_validation():  # test_drivers.cpp:254-262
+def test_config_validation(F):
     A = small_instance(3, 12, 3)
-    with pytest.raises(O.InvalidArgument):
-        O.feast_solve(A, I11, O.SolverConfig(m0=0))
-    with pytest.raises(O.InvalidArgument):
-        O.feast_solve(A, I11, O.SolverConfig(m0=4, tol=0.0))
+    with pytest.raises(F.InvalidArgument):
+        F.feast_solve(A, I11, F.SolverConfig(m0=0))
+    with pytest.raises(F.InvalidArgument):
+        F.feast_solve(A, I11, F.SolverConfig(m0=4, tol=0.0))
 
 
-def test_acceptance_c4_all_drivers():  # acceptance.cpp:136-195
+def test_acceptance_c4_all_drivers(F):
     for k in range(10):
         dense = k % 2 == 1
         n = 24 + 8 * (k % 5)
@@ -197,8 +197,8 @@ def test_acceptance_c4_all_drivers():  # acceptance.cpp:136-195
         scale = np.linalg.norm(A)
         w, V = O.dense_eig(A)
         Vin = V[:, [i for i in range(n) if I11.contains(w[i])]]
-        cfg = O.SolverConfig(m0=m + 4, n_c=8, s=3, tol=1e-9, max_iter=50, seed=6000 + k)
-        for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+        cfg = F.SolverConfig(m0=m + 4, n_c=8, s=3, tol=1e-9, max_iter=50, seed=6000 + k)
+        for d in (F.feast_solve, F.xfeast_solve, F.rfeast_solve):
             sol = d(A, I11, cfg)
             assert sol.converged
             assert len(sol.eigenvalues) == m_true
@@ -218,40 +218,40 @@ KBENCH = O.SearchInterval(-1.005, 1.005)
 
 
 @pytest.mark.slow
-def test_acceptance_c5_contrast():  # acceptance.cpp:199-244
+def test_acceptance_c5_contrast(F):
     sparse = _benchmark_family(False)
-    sol = O.feast_solve(sparse, KBENCH, O.SolverConfig(m0=75, n_c=3, tol=1e-10, max_iter=20,
+    sol = F.feast_solve(sparse, KBENCH, F.SolverConfig(m0=75, n_c=3, tol=1e-10, max_iter=20,
                                                        cache_factorizations=True))
     assert sol.converged and sol.iterations <= 20
     dense = _benchmark_family(True)
-    sol = O.feast_solve(dense, KBENCH, O.SolverConfig(m0=51, n_c=8, tol=1e-12, max_iter=10,
+    sol = F.feast_solve(dense, KBENCH, F.SolverConfig(m0=51, n_c=8, tol=1e-12, max_iter=10,
                                                       cache_factorizations=True))
     assert min(r.max_residual for r in sol.trace) > 1e-4
-    for d in (O.xfeast_solve, O.rfeast_solve):
-        sol = d(dense, KBENCH, O.SolverConfig(m0=51, n_c=8, s=3, tol=1e-6, max_iter=25,
+    for d in (F.xfeast_solve, F.rfeast_solve):
+        sol = d(dense, KBENCH, F.SolverConfig(m0=51, n_c=8, s=3, tol=1e-6, max_iter=25,
                                               cache_factorizations=True))
         assert sol.converged
 
 
-def test_acceptance_c7_clustered():  # acceptance.cpp:295-330
+def test_acceptance_c7_clustered(F):
     lay = O.SpectrumLayout(180, I11, 20, O.SearchInterval(1.05, 5.0), 160, "clustered", 4, 0.02, 77)
     A = O.assemble_matrix(*O.generate_spectrum(lay))
     I = O.SearchInterval(-1.005, 1.06)
-    cfg = O.SolverConfig(m0=44, n_c=8, tol=1e-13, max_iter=30, cache_factorizations=True)
-    r_feast = O.feast_solve(A, I, cfg).trace[-1].max_residual
+    cfg = F.SolverConfig(m0=44, n_c=8, tol=1e-13, max_iter=30, cache_factorizations=True)
+    r_feast = F.feast_solve(A, I, cfg).trace[-1].max_residual
     cfg.s = 3
-    for d in (O.xfeast_solve, O.rfeast_solve):
+    for d in (F.xfeast_solve, F.rfeast_solve):
         assert d(A, I, cfg).trace[-1].max_residual <= 1e-4 * r_feast
 
 
-def test_acceptance_c9_s1_equivalence():  # acceptance.cpp:390-425
+def test_acceptance_c9_s1_equivalence(F):
     for k in range(5):
         n = 24 + 4 * k
         lay = O.SpectrumLayout(n, O.SearchInterval(-0.9, 0.9), 5, O.SearchInterval(1.6, 12.0),
                                n - 5, seed=9000 + k)
         A = O.assemble_matrix(*O.generate_spectrum(lay))
-        cfg = O.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=15, seed=9100 + k)
-        f, x, r = (d(A, I11, cfg) for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve))
+        cfg = F.SolverConfig(m0=7, n_c=6, s=1, tol=1e-11, max_iter=15, seed=9100 + k)
+        f, x, r = (d(A, I11, cfg) for d in (F.feast_solve, F.xfeast_solve, F.rfeast_solve))
         assert len(f.trace) == len(x.trace) == len(r.trace)
         for a, b, c in zip(f.trace, x.trace, r.trace):
             tol = 1e-6 * a.max_residual + 1e-12
@@ -259,18 +259,18 @@ def test_acceptance_c9_s1_equivalence():  # acceptance.cpp:390-425
             assert abs(c.max_residual - a.max_residual) <= tol
 
 
-def test_acceptance_c10_determinism_accounting():  # acceptance.cpp:429-472
+def test_acceptance_c10_determinism_accounting(F):
     lay = O.SpectrumLayout(40, O.SearchInterval(-0.9, 0.9), 8, O.SearchInterval(1.4, 9.0), 32,
                            seed=1234)
     A = O.assemble_matrix(*O.generate_spectrum(lay))
-    cfg = O.SolverConfig(m0=11, n_c=5, s=3, tol=1e-13, max_iter=10)
-    for d in (O.feast_solve, O.xfeast_solve, O.rfeast_solve):
+    cfg = F.SolverConfig(m0=11, n_c=5, s=3, tol=1e-13, max_iter=10)
+    for d in (F.feast_solve, F.xfeast_solve, F.rfeast_solve):
         a, b = d(A, I11, cfg), d(A, I11, cfg)
-        assert O.write_trace_csv(a.trace) == O.write_trace_csv(b.trace)
+        assert F.write_trace_csv(a.trace) == F.write_trace_csv(b.trace)
         assert np.array_equal(a.eigenvalues, b.eigenvalues)
-    for rec in O.feast_solve(A, I11, cfg).trace:
+    for rec in F.feast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 11 * rec.iter
-    for rec in O.xfeast_solve(A, I11, cfg).trace:
+    for rec in F.xfeast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 11 * (rec.iter + 1)
-    for rec in O.rfeast_solve(A, I11, cfg).trace:
+    for rec in F.rfeast_solve(A, I11, cfg).trace:
         assert rec.rhs_cumulative == 5 * 11 * rec.iter

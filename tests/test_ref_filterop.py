@@ -1,28 +1,28 @@
-"""Oracle pin: re-expresses proj/tests/test_filterop.cpp and acceptance C2
-(proj/tests/acceptance.cpp:98-114) against the CPU oracle."""
+"""Re-expresses proj/tests/test_filterop.cpp and acceptance C2
+(proj/tests/acceptance.cpp:98-114) against both the CPU oracle (pin) and the B200 path (F = b200, -m gpu)."""
 import numpy as np
 import pytest
 
 import oracle as O
 
 
-def test_node_solve_trivial_cases():  # test_filterop.cpp:10-27
+def test_node_solve_trivial_cases(F):
     Z = np.zeros((3, 3))
     e1 = np.zeros((3, 1)); e1[0, 0] = 1.0
-    W = O.node_solve(Z, 1j, e1)
+    W = F.node_solve(Z, 1j, e1)
     assert abs(W[0, 0] - (-1j)) <= 1e-15
     assert abs(W[1, 0]) <= 1e-15
     D = np.diag([1.0, 2.0])
-    W2 = O.node_solve(D, 1 + 1j, np.ones((2, 1)))
+    W2 = F.node_solve(D, 1 + 1j, np.ones((2, 1)))
     assert abs(W2[0, 0] - (-1j)) <= 1e-14
     assert abs(W2[1, 0] - (-0.5 - 0.5j)) <= 1e-14
 
 
-def test_node_solve_residual():  # test_filterop.cpp:29-40
+def test_node_solve_residual(F):
     A = O.random_symmetric(12, 3)
     z = 0.37 + 0.5j
     X = O.random_block(12, 4, 4)
-    W = O.node_solve(A, z, X)
+    W = F.node_solve(A, z, X)
     S = -A.astype(complex) + z * np.eye(12)
     assert np.linalg.norm(S @ W - X) <= 1e-10 * np.linalg.norm(X)
 
@@ -42,109 +42,109 @@ def test_node_factor_pivots_on_modulus():
     np.testing.assert_allclose(L @ U, P @ S, atol=1e-13)
 
 
-def test_diagonal_matrix_reduces_to_scalar_filter():  # test_filterop.cpp:42-58
+def test_diagonal_matrix_reduces_to_scalar_filter(F):
     lams = np.array([-0.5, 0.3, 1.4, 6.0])
     A = np.diag(lams)
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 8)
-    acc = O.SolveAccounting()
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 8)
+    acc = F.SolveAccounting()
     for j in range(4):
         ej = np.zeros((4, 1)); ej[j, 0] = 1.0
-        Y = O.apply_filter(A, rule, ej, acc)
-        rho = O.filter_value(rule, lams[j])
+        Y = F.apply_filter(A, rule, ej, acc)
+        rho = F.filter_value(rule, lams[j])
         for i in range(4):
             assert abs(Y[i, 0] - (rho if i == j else 0.0)) <= 1e-13
     assert acc.rhs_solved == 32 and acc.factorizations == 32
 
 
-def test_eigenvector_maps_to_rho_times_itself():  # test_filterop.cpp:60-72
+def test_eigenvector_maps_to_rho_times_itself(F):
     A = O.random_symmetric(10, 11)
     w, V = O.dense_eig(A)
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 8)
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 8)
     for j in (0, 4, 9):
         x = V[:, [j]]
-        Y = O.apply_filter(A, rule, x)
-        assert np.abs(Y - O.filter_value(rule, w[j]) * x).max() <= 1e-12
+        Y = F.apply_filter(A, rule, x)
+        assert np.abs(Y - F.filter_value(rule, w[j]) * x).max() <= 1e-12
 
 
-def test_spectral_mapping_oracle():  # test_filterop.cpp:74-83
+def test_spectral_mapping_oracle(F):
     A = O.random_symmetric(16, 21)
-    rule = O.build_contour_rule(O.SearchInterval(-0.8, 0.9), 8)
+    rule = F.build_contour_rule(O.SearchInterval(-0.8, 0.9), 8)
     X = O.random_block(16, 3, 22)
-    Y = O.apply_filter(A, rule, X)
+    Y = F.apply_filter(A, rule, X)
     ref = O.spectral_filter_reference(A, rule, X)
     assert np.abs(Y - ref).max() <= 1e-10 * np.linalg.norm(X)
 
 
-def test_linearity():  # test_filterop.cpp:85-98
+def test_linearity(F):
     A = O.random_symmetric(14, 5)
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 6)
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 6)
     X1 = O.random_block(14, 2, 6)
     X2 = O.random_block(14, 2, 7)
     a, b = 0.7, -2.3
-    Y = O.apply_filter(A, rule, a * X1 + b * X2)
-    combo = a * O.apply_filter(A, rule, X1) + b * O.apply_filter(A, rule, X2)
+    Y = F.apply_filter(A, rule, a * X1 + b * X2)
+    combo = a * F.apply_filter(A, rule, X1) + b * F.apply_filter(A, rule, X2)
     assert np.abs(Y - combo).max() <= 1e-12 * np.abs(combo).max()
 
 
-def test_accounting_mixed_sequence():  # test_filterop.cpp:100-113
+def test_accounting_mixed_sequence(F):
     A = O.random_symmetric(9, 8)
-    acc = O.SolveAccounting()
+    acc = F.SolveAccounting()
     expected = 0
     for nc in (2, 5, 3):
-        rule = O.build_contour_rule(O.SearchInterval(-1, 1), nc)
+        rule = F.build_contour_rule(O.SearchInterval(-1, 1), nc)
         for p in (1, 4):
-            O.apply_filter(A, rule, O.random_block(9, p, nc * 10 + p), acc)
+            F.apply_filter(A, rule, O.random_block(9, p, nc * 10 + p), acc)
             expected += nc * p
     assert acc.rhs_solved == expected
 
 
-def test_deterministic_and_cache_invariant():  # test_filterop.cpp:115-133
+def test_deterministic_and_cache_invariant(F):
     A = O.random_symmetric(11, 13)
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 5)
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 5)
     X = O.random_block(11, 3, 14)
-    Y1 = O.apply_filter(A, rule, X)
-    Y2 = O.apply_filter(A, rule, X)
+    Y1 = F.apply_filter(A, rule, X)
+    Y2 = F.apply_filter(A, rule, X)
     assert np.array_equal(Y1, Y2)
-    acc = O.SolveAccounting()
-    Y4 = O.apply_filter(A, rule, X, acc, cache=True, napply=2)
+    acc = F.SolveAccounting()
+    Y4 = F.apply_filter(A, rule, X, acc, cache=True, napply=2)
     assert np.array_equal(Y4, Y1)
     assert acc.factorizations == 5
     assert acc.rhs_solved == 2 * 5 * 3
 
 
-def test_dimension_mismatch():  # test_filterop.cpp:135-141
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 2)
-    with pytest.raises(O.InvalidArgument):
-        O.apply_filter(np.eye(4), rule, np.zeros((3, 1)))
+def test_dimension_mismatch(F):
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 2)
+    with pytest.raises(F.InvalidArgument):
+        F.apply_filter(np.eye(4), rule, np.zeros((3, 1)))
 
 
-def test_acceptance_c2_projector_equivalence():  # acceptance.cpp:98-114
+def test_acceptance_c2_projector_equivalence(F):
     for k in range(20):
         n = 8 + (3 * k) % 25
         A = O.random_symmetric(n, 1000 + k)
-        rule = O.build_contour_rule(O.SearchInterval(-1, 1), 8)
+        rule = F.build_contour_rule(O.SearchInterval(-1, 1), 8)
         X = O.random_block(n, 3, 2000 + k)
-        Y = O.apply_filter(A, rule, X)
+        Y = F.apply_filter(A, rule, X)
         ref = O.spectral_filter_reference(A, rule, X)
         assert np.abs(Y - ref).max() <= 1e-10 * np.linalg.norm(X), k
 
 
-def test_blocked_lu_spans_multiple_panels():
+def test_blocked_lu_spans_multiple_panels(F):
     # n > the oracle's 64-wide panel: spectral-mapping oracle still holds
     A = O.random_symmetric(200, 99) / 10.0
-    rule = O.build_contour_rule(O.SearchInterval(-0.5, 0.5), 8)
+    rule = F.build_contour_rule(O.SearchInterval(-0.5, 0.5), 8)
     X = O.random_block(200, 5, 98)
-    Y = O.apply_filter(A, rule, X)
+    Y = F.apply_filter(A, rule, X)
     ref = O.spectral_filter_reference(A, rule, X)
     assert np.abs(Y - ref).max() <= 1e-10 * np.linalg.norm(X)
 
 
-def test_singular_node_reports_index():
+def test_singular_node_reports_index(F):
     # A = diag(0, 1), contour node z exactly at an eigenvalue is impossible for
     # a real A (Im z > 0) unless via external nodes; an exactly singular shift
     # arises with z = i and A = [[0, 1], [-1, 0]] which is not symmetric, so
     # use an overflow: non-finite entries make |U_ii| non-finite.
     A = np.array([[np.inf, 0.0], [0.0, 1.0]])
-    rule = O.build_contour_rule(O.SearchInterval(-1, 1), 2)
-    with pytest.raises(O.FeastRuntimeError):
-        O.apply_filter(A, rule, np.ones((2, 1)))
+    rule = F.build_contour_rule(O.SearchInterval(-1, 1), 2)
+    with pytest.raises(F.FeastRuntimeError):
+        F.apply_filter(A, rule, np.ones((2, 1)))
