@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""FEAST rational-filter hot path benchmark (BASELINE.json metric).
+
+One step = one FilterApplier::apply (proj/src/filterop.cpp:62-84) on the
+workload: shift + complex partial-pivot LU + m0-RHS solve per contour node,
+ascending-node weighted accumulation (+ NCCL all-reduce across ranks when the
+nodes are sharded). value = filter FP64 GFLOP/s of the whole job,
+F_filter = n_c (8/3 n^3 + 8 n^2 m0) per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+
+Under torchrun (N > 1) each rank owns n_c/N contiguous nodes; timing is the
+max over ranks of CUDA-event time on the library stream. --impl reference
+times the CPU oracle (the reference's algorithm restated on OpenBLAS; the
+reference itself needs Eigen, which is absent) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FEAST time-to-solution and filter-solve FP64 GFLOP/s vs FP64 peak, 1/2/4/8 GPU"
+# FP64 DMMA peak measured on this pool's B200 by tools/fp64_peak.cu (profiles/fp64_peak.json);
+# MEASURED_PEAKS.json carries no FP64 entry.
+FP64_DMMA_PEAK_TFLOPS = 37.08
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-tts", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def filter_flops(n, p, nc):
+    return nc * (8.0 / 3.0 * n ** 3 + 8.0 * n * n * p)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        under = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(under), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(cfg_index, device):
+    """Seeded synthetic A = Q diag(Lambda) Q^T of the config (fixture, outside
+    the timed region): Lambda from the product's mt19937_64 fills, Q by a
+    device Householder QR (torch.linalg.qr) of the seeded Gaussian block."""
+    import torch
+
+    import paper_1605_08771_b200 as P
+    from paper_1605_08771_b200 import configs as CF
+
+    vals = CF.spectrum(cfg_index, P.uniform_values)
+    c = CF.resolved(cfg_index, vals)
+    n = c["n"]
+    dev = torch.device("cuda", device)
+    if cfg_index == 3:
+        A = torch.from_numpy(CF.laplacian_2d()).to(dev)
+    else:
+        G = torch.from_numpy(P.gaussian_block(n, n, 1000 + cfg_index)).to(dev)
+        Q, _ = torch.linalg.qr(G)
+        imax = Q.abs().argmax(dim=0)
+        sgn = torch.sign(Q[imax, torch.arange(n, device=dev)])
+        Q = Q * sgn
+        A = (Q * torch.from_numpy(vals).to(dev)) @ Q.T
+        A = 0.5 * (A + A.T)
+        del G, Q
+    A = A.contiguous()  # row-major storage of a symmetric matrix == column-major
+    return A, vals, c
+
+
+def cpu_sample(c, threads):
+    """Oracle (restated reference algorithm) on one contour node of the workload:
+    one zI - A LU + m0-RHS solve + accumulation = F_filter / n_c flops."""
+    import oracle as O
+    from paper_1605_08771_b200 import configs as CF  # noqa: F401
+
+    O.set_threads(threads)
+    n, p = c["n"], c["m0"]
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((n, n))
+    A = np.asfortranarray(0.5 * (M + M.T) / np.sqrt(n))
+    X = np.asfortranarray(rng.standard_normal((n, p)))
+    rule = O.build_contour_rule(O.SearchInterval(c["lo"], c["hi"]), c["n_c"])
+    one = O.ContourRule(rule.interval, rule.nodes[:1], rule.weights[:1])
+    t0 = time.perf_counter()
+    O.apply_filter(A, one, X)
+    dt = time.perf_counter() - t0
+    flops = filter_flops(n, p, 1)
+    return flops / dt / 1e9, dt
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle as O  # noqa: F401
+    from paper_1605_08771_b200 import configs as CF
+    import paper_1605_08771_b200 as P
+
+    vals = CF.spectrum(args.config, P.uniform_values)
+    c = CF.resolved(args.config, vals)
+    threads = os.cpu_count() or 1
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample(c, threads)
+    rates = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        r, dt = cpu_sample(c, threads)
+        rates.append(r)
+        t_all += dt
+    value = float(np.mean(rates))
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_all / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic",
+        "config": {"workload": CF.CONFIGS[args.config].name, "n": c["n"], "m0": c["m0"],
+                   "n_c": c["n_c"]},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port",
+                         "sample": "one contour node per step (zI-A LU + m0-RHS solve + "
+                                   "accumulate) of the workload, oracle restatement of "
+                                   "proj/src/filterop.cpp on OpenBLAS; reference (Eigen) "
+                                   "unbuildable here"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    import paper_1605_08771_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        uid = P.Context.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        ctx = P.Context(local_rank, nccl_id=bytes(t.tolist()), rank=rank, nranks=world)
+    else:
+        ctx = P.Context(local_rank)
+    P.set_default_context(ctx)
+
+    A, vals, c = build_workload(args.config, local_rank)
+    n, p, nc = c["n"], c["m0"], c["n_c"]
+    X0 = P.make_initial_guess(n, p, 42)
+    dev = torch.device("cuda", local_rank)
+    X = torch.from_numpy(np.ascontiguousarray(X0.T)).to(dev)   # (p, n) row-major == n x p col-major
+    Y = torch.empty((p, n), dtype=torch.float64, device=dev)
+    dA = P.DeviceMatrix.from_device(A.data_ptr(), n, n, ctx)
+    rule = P.build_contour_rule(P.SearchInterval(c["lo"], c["hi"]), nc)
+    filt = P.FilterApplier(None, rule, False, ctx=ctx, device_matrix=dA)
+    torch.cuda.synchronize()
+    del A
+    torch.cuda.empty_cache()
+
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    acc = P.SolveAccounting()
+
+    def step():
+        filt.apply_device(X.data_ptr(), n, p, Y.data_ptr(), n, acc)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ctx.set_profiling(True)
+    l0 = ctx.launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    launches = ctx.launches() - l0
+    ms = e0.elapsed_time(e1)
+    prof = {k: ctx.profile(k) for k in P.Context.KERNEL_CLASSES}
+    ctx.set_profiling(False)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_flops = filter_flops(n, p, nc) * args.steps
+    value = total_flops / (ms * 1e-3) / 1e9
+
+    # e2e: pinned host buffers through the same public API (H2D of X, D2H of Y inside)
+    Xh = torch.empty((p, n), dtype=torch.float64, pin_memory=True).numpy().T  # n x p, col-major
+    Yh = torch.empty((p, n), dtype=torch.float64, pin_memory=True).numpy().T
+    Xh[...] = X0
+    filt.apply(Xh, acc, out=Yh)  # warm
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        filt.apply(Xh, acc, out=Yh)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = total_flops / e2e_s / 1e9
+
+    # time-to-solution: full feast_solve (host A in, Solution out) once
+    tts = None
+    if not args.no_tts and rank == 0 and world == 1:
+        Ah = None
+        try:
+            A2, _, _ = build_workload(args.config, local_rank)
+            Ah = A2.cpu().numpy().T.copy(order="F")
+            del A2
+            torch.cuda.empty_cache()
+            S = P.SymmetricMatrix(Ah)
+            cfg = P.SolverConfig(m0=p, n_c=nc, tol=c["tol"], max_iter=c["max_iter"])
+            t0 = time.perf_counter()
+            sol = P.feast_solve(S, P.SearchInterval(c["lo"], c["hi"]), cfg, ctx=ctx)
+            tts = {"seconds": round(time.perf_counter() - t0, 4), "iterations": sol.iterations,
+                   "converged": sol.converged, "eigenpairs": len(sol.eigenvalues),
+                   "expected_inside": c["inside"],
+                   "max_residual": sol.trace[-1].max_residual if sol.trace else None,
+                   "cache_factorizations": False}
+        except Exception as e:  # report, do not hide
+            tts = {"error": f"{type(e).__name__}: {e}"}
+
+    if rank != 0:
+        return
+    zms, zflops, zl = prof["zgemm"]
+    total_ms_prof = sum(v[0] for v in prof.values())
+    achieved = zflops / (zms * 1e-3) / 1e12 if zms > 0 else 0.0
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            threads = os.cpu_count() or 1
+            rate, dt = cpu_sample(c, threads)
+            cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                   "sample": f"one contour node (n={n}, m0={p}) of the workload: LU + solve + "
+                             f"accumulate in {dt:.2f} s, oracle restatement on OpenBLAS"}
+        except Exception as e:
+            cpu = {"error": f"{type(e).__name__}: {e}"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128/f64 (DMMA m8n8k4 f64)", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}", "name": f"{n}x{n} dense, m0={p}, n_c={nc}",
+                   "n": n, "m0": p, "n_c": nc, "interval": [c["lo"], c["hi"]],
+                   "parallelism": f"contour nodes sharded {nc}/{world} per GPU + NCCL allreduce",
+                   "l2": "inputs larger than L2 (n_c LU factors, 16 n^2 B each)"},
+        "fraction_of_fp64_peak": round(value / 1e3 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
+        "roofline": {"kernel": "zgemm_sub_kernel (LU trailing update + blocked solves)",
+                     "bound": "tensor", "achieved": round(achieved, 3),
+                     "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
+                     "traffic": None,
+                     "peak_source": "measured FP64 DMMA burst, tools/fp64_peak.cu "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "share_of_step": round(zms / total_ms_prof, 4) if total_ms_prof else None,
+                     "launches": zl},
+        "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 3),
+                        "work_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
+                    for k, v in prof.items()},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": 8 * n * p, "d2h_bytes_per_step": 8 * n * p},
+        "gpu_launches": int(launches),
+        "cpu_baseline": cpu,
+        "tts": tts,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,12 @@ void* fl_ctx_stream(fl_ctx* ctx); /* cudaStream_t */
 int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks);
 /* number of kernels this context launched so far (instrumentation) */
 long long fl_ctx_launches(const fl_ctx* ctx);
+/* per-kernel-class CUDA-event timing on the context stream (instrumentation):
+   classes "shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
+   "allreduce"; work = algorithmic flops (GEMM/TRSM) or bytes (streams). */
+int fl_ctx_set_profiling(fl_ctx* ctx, int on);
+int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,
+                   fl_err* err);
 
 /* ------------------------------------------------------------ matrix
    SymmetricMatrix (proj/include/feastlab/matmodel.hpp:12-24): the caller has

@@ -86,6 +86,40 @@ struct DBuf {
     int* i() const { return static_cast<int*>(p); }
 };
 
+// Per-kernel-class CUDA-event timing (fl_ctx_set_profiling): bench.py's
+// roofline numbers come from these events, recorded on the launch stream.
+enum ProfClass { P_SHIFT, P_PANEL, P_LASWP, P_TRSM, P_ZGEMM, P_PERMUTE, P_ACCUM, P_ALLREDUCE,
+                 P_NCLASS };
+const char* const kProfNames[P_NCLASS] = {"shift",   "panel",      "laswp",    "trsm",
+                                          "zgemm",   "permute",    "accumulate", "allreduce"};
+
+struct Profiler {
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        double work;
+    };
+    bool on = false;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void reset() {
+        recs.clear();
+        used = 0;
+    }
+    ~Profiler() {
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
+};
+
 }  // namespace
 
 struct fl_ctx {
@@ -95,6 +129,7 @@ struct fl_ctx {
     ncclComm_t comm = nullptr;
     std::recursive_mutex mu;
     long long launches_at_create = 0;
+    Profiler prof;
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
         scal;
@@ -188,6 +223,28 @@ void copy_out(fl_ctx* ctx, double* dst, long ldd, int n, const double* src, long
 
 void sync(fl_ctx* ctx) { CK(cudaStreamSynchronize(ctx->stream)); }
 
+// --------------------------------------------------------------- profiling scope
+struct Prof {
+    fl_ctx* ctx;
+    int cls;
+    double work;
+    cudaEvent_t a = nullptr;
+    Prof(fl_ctx* c, int k, double w, int launches = 1) : ctx(c), cls(k), work(w) {
+        g_launch_count += launches;
+        if (ctx->prof.on) {
+            a = ctx->prof.get();
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~Prof() {
+        if (a) {
+            cudaEvent_t b = ctx->prof.get();
+            cudaEventRecord(b, ctx->stream);
+            ctx->prof.recs.push_back({cls, a, b, work});
+        }
+    }
+};
+
 // --------------------------------------------------------------- filter core
 // Factor nodes [g0, g0+G) of the local range into factor slots [s0, s0+G).
 void factor_group(fl_filter* f, int g0, int G, int s0) {
@@ -201,27 +258,37 @@ void factor_group(fl_filter* f, int g0, int G, int s0) {
         z.zi[b] = f->zi[f->kb + g0 + b];
     }
     int* ipiv = f->ipiv.i() + (long)s0 * N;
-    launch_shift(f->A->d(), N, N, F, z, G, ctx->stream);
-    g_launch_count += 1;
+    {
+        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G);
+        launch_shift(f->A->d(), N, N, F, z, G, ctx->stream);
+    }
     for (int k0 = 0; k0 < N; k0 += FL_TILE) {
-        launch_panel(F, N, k0, ipiv, G, ctx->stream);
-        launch_laswp_panel(F, N, k0, ipiv, G, ctx->stream);
-        g_launch_count += 2;
+        {
+            Prof pr(ctx, P_PANEL, 0.0);
+            launch_panel(F, N, k0, ipiv, G, ctx->stream);
+        }
+        {
+            Prof pr(ctx, P_LASWP, 0.0);
+            launch_laswp_panel(F, N, k0, ipiv, G, ctx->stream);
+        }
         const int rest = N - k0 - FL_TILE;
         if (rest > 0) {
-            launch_trsm_unit_lower(F, k0, F, k0, k0 + FL_TILE, rest, G, ctx->stream);
+            {
+                Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * rest * G);
+                launch_trsm_unit_lower(F, k0, F, k0, k0 + FL_TILE, rest, G, ctx->stream);
+            }
             ZGemm g{rest, rest, FL_TILE,
                     F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N, stride,
                     F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0, N, stride,
                     F.re + (long)(k0 + FL_TILE) * N + k0 + FL_TILE,
                     F.im + (long)(k0 + FL_TILE) * N + k0 + FL_TILE, N, stride};
+            Prof pr(ctx, P_ZGEMM, 8.0 * rest * rest * FL_TILE * G);
             launch_zgemm_sub(g, G, ctx->stream);
-            g_launch_count += 2;
         }
     }
+    Prof pr(ctx, P_PANEL, 0.0, 2);
     launch_check_diag(F, n, G, g0, f->bad.i(), ctx->stream);
     launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, ctx->stream);
-    g_launch_count += 2;
 }
 
 // W_b = (z_b I - A)^{-1} X for nodes [g0, g0+G) using factor slots [s0, ...).
@@ -231,34 +298,40 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
     const long stride = (long)N * N;
     ZBatch F{f->fac_re.d() + s0 * stride, f->fac_im.d() + s0 * stride, N, stride};
     ZBatch W{f->w_re.d() + g0 * f->w_stride, f->w_im.d() + g0 * f->w_stride, N, f->w_stride};
-    launch_permute_rhs(X, ldx, N, P, f->perm.i() + (long)s0 * N, W, G, ctx->stream);
-    g_launch_count += 1;
+    {
+        Prof pr(ctx, P_PERMUTE, 24.0 * N * P * G);
+        launch_permute_rhs(X, ldx, N, P, f->perm.i() + (long)s0 * N, W, G, ctx->stream);
+    }
     const int NB = N / FL_TILE;
     for (int ib = 0; ib < NB; ++ib) {  // forward, unit lower
         const int r0 = ib * FL_TILE;
-        launch_trsm_unit_lower(F, r0, W, r0, 0, P, G, ctx->stream);
+        {
+            Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * P * G);
+            launch_trsm_unit_lower(F, r0, W, r0, 0, P, G, ctx->stream);
+        }
         const int rest = N - r0 - FL_TILE;
-        g_launch_count += 1;
         if (rest > 0) {
             ZGemm g{rest, P, FL_TILE,
                     F.re + (long)r0 * N + r0 + FL_TILE, F.im + (long)r0 * N + r0 + FL_TILE, N, stride,
                     W.re + r0, W.im + r0, N, W.stride,
                     W.re + r0 + FL_TILE, W.im + r0 + FL_TILE, N, W.stride};
+            Prof pr(ctx, P_ZGEMM, 8.0 * rest * P * FL_TILE * G);
             launch_zgemm_sub(g, G, ctx->stream);
-            g_launch_count += 1;
         }
     }
     for (int ib = NB - 1; ib >= 0; --ib) {  // backward, upper
         const int r0 = ib * FL_TILE;
-        launch_trsm_upper(F, r0, W, r0, 0, P, G, ctx->stream);
-        g_launch_count += 1;
+        {
+            Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * P * G);
+            launch_trsm_upper(F, r0, W, r0, 0, P, G, ctx->stream);
+        }
         if (r0 > 0) {
             ZGemm g{r0, P, FL_TILE,
                     F.re + (long)r0 * N, F.im + (long)r0 * N, N, stride,
                     W.re + r0, W.im + r0, N, W.stride,
                     W.re, W.im, N, W.stride};
+            Prof pr(ctx, P_ZGEMM, 8.0 * r0 * P * FL_TILE * G);
             launch_zgemm_sub(g, G, ctx->stream);
-            g_launch_count += 1;
         }
     }
 }
@@ -385,13 +458,14 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     }
     ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
     if (L > 0) {
+        Prof pr(ctx, P_ACCUM, (16.0 * L + 8.0) * N * P);
         launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
-        g_launch_count += 1;
     } else {
         CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
     }
     if (ctx->nranks > 1) {
         if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
+        Prof pr(ctx, P_ALLREDUCE, 8.0 * N * p, 0);
         nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm, ctx->stream),
                    "ncclAllReduce(Y)");
     }
@@ -677,6 +751,38 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 }
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
+
+int fl_ctx_set_profiling(fl_ctx* ctx, int on) {
+    CtxLock lk(ctx);
+    ctx->prof.on = on != 0;
+    ctx->prof.reset();
+    return FL_OK;
+}
+
+int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,
+                   fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        int k = -1;
+        for (int i = 0; i < P_NCLASS; ++i)
+            if (std::strcmp(cls, kProfNames[i]) == 0) k = i;
+        if (k < 0) throw Fail{FL_INVALID_ARGUMENT, std::string("unknown kernel class ") + cls};
+        sync(ctx);
+        double t = 0.0, w = 0.0;
+        long long c = 0;
+        for (const auto& r : ctx->prof.recs) {
+            if (r.cls != k) continue;
+            float e = 0.f;
+            CK(cudaEventElapsedTime(&e, r.a, r.b));
+            t += e;
+            w += r.work;
+            ++c;
+        }
+        *ms = t;
+        *work = w;
+        *launches = c;
+    });
+}
 
 int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_matrix** out,
                      fl_err* err) {

@@ -10,7 +10,7 @@
 #include <cooperative_groups.h>
 
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 
 #include "common.cuh"
@@ -22,12 +22,15 @@ namespace fl {
 
 void ensure_smem(const void* func, size_t bytes) {
     static std::mutex mu;
-    static std::set<std::pair<const void*, int>> done;
+    static std::map<std::pair<const void*, int>, size_t> done;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
-    if (done.insert({func, dev}).second)
+    size_t& have = done[{func, dev}];
+    if (bytes > have) {
         cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        have = bytes;
+    }
 }
 
 // ------------------------------------------------------------------ shift

@@ -109,6 +109,20 @@ class Context:
     def launches(self) -> int:
         return L.lib().fl_ctx_launches(self.handle)
 
+    KERNEL_CLASSES = ("shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
+                      "allreduce")
+
+    def set_profiling(self, on: bool) -> None:
+        """Per-kernel-class CUDA-event timing on the context stream."""
+        L.lib().fl_ctx_set_profiling(self.handle, int(bool(on)))
+
+    def profile(self, cls: str):
+        """(milliseconds, algorithmic work, launches) accumulated for `cls`."""
+        ms, work, n = C.c_double(), C.c_double(), C.c_longlong()
+        _call(L.lib().fl_ctx_profile, self.handle, cls.encode(), C.byref(ms), C.byref(work),
+              C.byref(n))
+        return ms.value, work.value, n.value
+
     def close(self):
         if self.handle:
             L.lib().fl_ctx_destroy(self.handle)
@@ -351,7 +365,7 @@ class FilterApplier:
               C.byref(h))
         self.handle = h
 
-    def apply(self, X, accounting: SolveAccounting | None = None) -> np.ndarray:
+    def apply(self, X, accounting: SolveAccounting | None = None, out=None) -> np.ndarray:
         X = _f64(X)
         if X.ndim == 1:
             X = X.reshape(-1, 1, order="F")
@@ -363,7 +377,9 @@ class FilterApplier:
         acc = accounting if accounting is not None else SolveAccounting()
         rhs = C.c_longlong(acc.rhs_solved)
         facts = C.c_longlong(acc.factorizations)
-        Y = np.zeros(X.shape, order="F")
+        Y = out if out is not None else np.zeros(X.shape, order="F")
+        if Y.shape != X.shape or not Y.flags.f_contiguous or Y.dtype != np.float64:
+            raise InvalidArgument("apply: out must be a Fortran-ordered float64 array like X")
         _call(L.lib().fl_filter_apply_raw, self.handle, _ptr(X), X.shape[0], X.shape[1], _ptr(Y),
               Y.shape[0], L.FL_HOST, C.byref(rhs), C.byref(facts))
         acc.rhs_solved, acc.factorizations = rhs.value, facts.value

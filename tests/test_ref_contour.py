@@ -100,9 +100,9 @@ def test_predicted_rate(F):
     spec = [-0.7, 0.1, 0.6, 2.4]
     expected = F.filter_value(r, 2.4) / F.filter_value(r, -0.7)
     assert O.predicted_rate(r, spec, 3) == pytest.approx(expected, rel=1e-14)
-    with pytest.raises(F.InvalidArgument):
+    with pytest.raises(O.InvalidArgument):
         O.predicted_rate(r, spec, 4)
-    with pytest.raises(F.InvalidArgument):
+    with pytest.raises(O.InvalidArgument):
         O.predicted_rate(r, spec, 0)
 
 
@@ -119,8 +119,8 @@ def test_external_nodes(F):
 
 def test_interval(F):
     with pytest.raises(F.InvalidArgument):
-        O.SearchInterval(1.0, 1.0)
+        F.SearchInterval(1.0, 1.0)
     with pytest.raises(F.InvalidArgument):
-        O.SearchInterval(2.0, -1.0)
-    I = O.SearchInterval(-1, 1)
+        F.SearchInterval(2.0, -1.0)
+    I = F.SearchInterval(-1, 1)
     assert I.contains(0.0) and not I.contains(1.0) and not I.contains(-1.0)
