@@ -130,6 +130,9 @@ struct fl_ctx {
     std::recursive_mutex mu;
     long long launches_at_create = 0;
     Profiler prof;
+    std::vector<cudaStream_t> aux;  // node-chunk streams (fork/join on `stream`)
+    cudaEvent_t fork = nullptr;
+    std::vector<cudaEvent_t> join;
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
         scal;
@@ -161,6 +164,7 @@ struct fl_filter {
     int kb = 0, ke = 0;  // local node range [kb, ke)
     // factors: cache -> one per local node; else a rotating group
     DBuf fac_re, fac_im, ipiv, perm, bad;
+    DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     int fac_slots = 0;
     std::vector<char> factored;  // cache mode, per local node
     DBuf w_re, w_im;             // W for all local nodes (N x P each)
@@ -228,18 +232,20 @@ struct Prof {
     fl_ctx* ctx;
     int cls;
     double work;
+    cudaStream_t st;
     cudaEvent_t a = nullptr;
-    Prof(fl_ctx* c, int k, double w, int launches = 1) : ctx(c), cls(k), work(w) {
+    Prof(fl_ctx* c, int k, double w, int launches = 1, cudaStream_t s = nullptr)
+        : ctx(c), cls(k), work(w), st(s ? s : c->stream) {
         g_launch_count += launches;
         if (ctx->prof.on) {
             a = ctx->prof.get();
-            cudaEventRecord(a, ctx->stream);
+            cudaEventRecord(a, st);
         }
     }
     ~Prof() {
         if (a) {
             cudaEvent_t b = ctx->prof.get();
-            cudaEventRecord(b, ctx->stream);
+            cudaEventRecord(b, st);
             ctx->prof.recs.push_back({cls, a, b, work});
         }
     }
@@ -247,7 +253,7 @@ struct Prof {
 
 // --------------------------------------------------------------- filter core
 // Factor nodes [g0, g0+G) of the local range into factor slots [s0, s0+G).
-void factor_group(fl_filter* f, int g0, int G, int s0) {
+void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
     fl_ctx* ctx = f->ctx;
     const int N = f->A->N, n = f->A->n;
     const long stride = (long)N * N;
@@ -258,80 +264,98 @@ void factor_group(fl_filter* f, int g0, int G, int s0) {
         z.zi[b] = f->zi[f->kb + g0 + b];
     }
     int* ipiv = f->ipiv.i() + (long)s0 * N;
+    const int NB = N / FL_TILE;
+    const long istride = 2L * NB * FL_TILE * FL_TILE;
+    ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
     {
-        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G);
-        launch_shift(f->A->d(), N, N, F, z, G, ctx->stream);
+        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
+        launch_shift(f->A->d(), N, N, F, z, G, st);
     }
     for (int k0 = 0; k0 < N; k0 += FL_TILE) {
         {
-            Prof pr(ctx, P_PANEL, 0.0);
-            launch_panel(F, N, k0, ipiv, G, ctx->stream);
+            Prof pr(ctx, P_PANEL, 0.0, 2, st);
+            launch_panel(F, N, k0, ipiv, G, st);
+            launch_trinv(F, k0, 1, false, Inv, k0 / FL_TILE, G, st);
         }
         {
-            Prof pr(ctx, P_LASWP, 0.0);
-            launch_laswp_panel(F, N, k0, ipiv, G, ctx->stream);
+            Prof pr(ctx, P_LASWP, 0.0, 1, st);
+            launch_laswp_panel(F, N, k0, ipiv, G, st);
         }
         const int rest = N - k0 - FL_TILE;
         if (rest > 0) {
             {
-                Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * rest * G);
-                launch_trsm_unit_lower(F, k0, F, k0, k0 + FL_TILE, rest, G, ctx->stream);
+                // U12 = L11^{-1} A12, in place
+                Prof pr(ctx, P_TRSM, 8.0 * FL_TILE * FL_TILE * rest * G, 1, st);
+                ZGemm u{FL_TILE, rest, FL_TILE,
+                        Inv.re + (long)(k0 / FL_TILE) * FL_TILE * FL_TILE,
+                        Inv.im + (long)(k0 / FL_TILE) * FL_TILE * FL_TILE, FL_TILE, Inv.stride,
+                        F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0,
+                        N, stride,
+                        F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0,
+                        N, stride};
+                launch_zgemm_set(u, G, st);
             }
             ZGemm g{rest, rest, FL_TILE,
                     F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N, stride,
                     F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0, N, stride,
                     F.re + (long)(k0 + FL_TILE) * N + k0 + FL_TILE,
                     F.im + (long)(k0 + FL_TILE) * N + k0 + FL_TILE, N, stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * rest * rest * FL_TILE * G);
-            launch_zgemm_sub(g, G, ctx->stream);
+            Prof pr(ctx, P_ZGEMM, 8.0 * rest * rest * FL_TILE * G, 1, st);
+            launch_zgemm_sub(g, G, st);
         }
     }
-    Prof pr(ctx, P_PANEL, 0.0, 2);
-    launch_check_diag(F, n, G, g0, f->bad.i(), ctx->stream);
-    launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, ctx->stream);
+    Prof pr(ctx, P_PANEL, 0.0, 3, st);
+    launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
+    launch_check_diag(F, n, G, g0, f->bad.i(), st);
+    launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, st);
 }
 
 // W_b = (z_b I - A)^{-1} X for nodes [g0, g0+G) using factor slots [s0, ...).
-void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx, int P) {
+void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx, int P,
+                 cudaStream_t st) {
     fl_ctx* ctx = f->ctx;
     const int N = f->A->N;
     const long stride = (long)N * N;
     ZBatch F{f->fac_re.d() + s0 * stride, f->fac_im.d() + s0 * stride, N, stride};
     ZBatch W{f->w_re.d() + g0 * f->w_stride, f->w_im.d() + g0 * f->w_stride, N, f->w_stride};
     {
-        Prof pr(ctx, P_PERMUTE, 24.0 * N * P * G);
-        launch_permute_rhs(X, ldx, N, P, f->perm.i() + (long)s0 * N, W, G, ctx->stream);
+        Prof pr(ctx, P_PERMUTE, 24.0 * N * P * G, 1, st);
+        launch_permute_rhs(X, ldx, N, P, f->perm.i() + (long)s0 * N, W, G, st);
     }
     const int NB = N / FL_TILE;
+    const long istride = 2L * NB * FL_TILE * FL_TILE;
+    ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
+    auto tri = [&](int blk, int r0) {  // W_i <- T_ii^{-1} W_i (DMMA, in place)
+        Prof pr(ctx, P_TRSM, 8.0 * FL_TILE * FL_TILE * P * G, 1, st);
+        ZGemm u{FL_TILE, P, FL_TILE,
+                Inv.re + (long)blk * FL_TILE * FL_TILE, Inv.im + (long)blk * FL_TILE * FL_TILE,
+                FL_TILE, Inv.stride,
+                W.re + r0, W.im + r0, N, W.stride, W.re + r0, W.im + r0, N, W.stride};
+        launch_zgemm_set(u, G, st);
+    };
     for (int ib = 0; ib < NB; ++ib) {  // forward, unit lower
         const int r0 = ib * FL_TILE;
-        {
-            Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * P * G);
-            launch_trsm_unit_lower(F, r0, W, r0, 0, P, G, ctx->stream);
-        }
+        tri(ib, r0);
         const int rest = N - r0 - FL_TILE;
         if (rest > 0) {
             ZGemm g{rest, P, FL_TILE,
                     F.re + (long)r0 * N + r0 + FL_TILE, F.im + (long)r0 * N + r0 + FL_TILE, N, stride,
                     W.re + r0, W.im + r0, N, W.stride,
                     W.re + r0 + FL_TILE, W.im + r0 + FL_TILE, N, W.stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * rest * P * FL_TILE * G);
-            launch_zgemm_sub(g, G, ctx->stream);
+            Prof pr(ctx, P_ZGEMM, 8.0 * rest * P * FL_TILE * G, 1, st);
+            launch_zgemm_sub(g, G, st);
         }
     }
     for (int ib = NB - 1; ib >= 0; --ib) {  // backward, upper
         const int r0 = ib * FL_TILE;
-        {
-            Prof pr(ctx, P_TRSM, 4.0 * FL_TILE * FL_TILE * P * G);
-            launch_trsm_upper(F, r0, W, r0, 0, P, G, ctx->stream);
-        }
+        tri(NB + ib, r0);
         if (r0 > 0) {
             ZGemm g{r0, P, FL_TILE,
                     F.re + (long)r0 * N, F.im + (long)r0 * N, N, stride,
                     W.re + r0, W.im + r0, N, W.stride,
                     W.re, W.im, N, W.stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * r0 * P * FL_TILE * G);
-            launch_zgemm_sub(g, G, ctx->stream);
+            Prof pr(ctx, P_ZGEMM, 8.0 * r0 * P * FL_TILE * G, 1, st);
+            launch_zgemm_sub(g, G, st);
         }
     }
 }
@@ -374,59 +398,62 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->fac_im.ensure(sizeof(double) * (size_t)fstride * slots);
         f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
         f->perm.ensure(sizeof(int) * (size_t)N * slots);
+        f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
+        f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->fac_slots = slots;
         std::fill(f->factored.begin(), f->factored.end(), 0);
     }
     f->bad.ensure(sizeof(int) * 4);
     int big = 0x7fffffff;
     CK(cudaMemcpyAsync(f->bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    // Node chunks run concurrently on the context's auxiliary streams so one
+    // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
+    const int ns = std::max(1, std::min<int>(std::min(L, slots), (int)ctx->aux.size()));
+    CK(cudaEventRecord(ctx->fork, ctx->stream));
+    for (int j = 0; j < ns; ++j) CK(cudaStreamWaitEvent(ctx->aux[j], ctx->fork, 0));
     long long new_facts = 0;
     if (f->cache) {
-        // factor the not-yet-cached nodes in contiguous runs
-        int g = 0;
-        while (g < L) {
-            if (f->factored[g]) { ++g; continue; }
-            int e = g;
-            while (e < L && !f->factored[e] && e - g < 16) ++e;
-            factor_group(f, g, e - g, g);
-            // slot-relative bad index -> local node index
-            for (int k = g; k < e; ++k) f->factored[k] = 1;
-            new_facts += e - g;
-            g = e;
+        // chunk j = nodes [j*L/ns, (j+1)*L/ns); factor the uncached ones, then solve
+        for (int j = 0; j < ns; ++j) {
+            const int c0 = (int)((long)L * j / ns), c1 = (int)((long)L * (j + 1) / ns);
+            int g = c0;
+            while (g < c1) {
+                if (f->factored[g]) { ++g; continue; }
+                int e = g;
+                while (e < c1 && !f->factored[e]) ++e;
+                factor_group(f, g, e - g, g, ctx->aux[j]);
+                for (int k = g; k < e; ++k) f->factored[k] = 1;
+                new_facts += e - g;
+                g = e;
+            }
+            if (c1 > c0) solve_group(f, c0, c1 - c0, c0, X, ldx, P, ctx->aux[j]);
         }
-        solve_group(f, 0, L, 0, X, ldx, P);
     } else {
+        // rounds of `slots` nodes; round chunk j reuses slots [j*slots/ns, ...) on stream j
         for (int g = 0; g < L; g += slots) {
             const int G = std::min(slots, L - g);
-            // bad index is relative to the group; offset by shifting the flag base
-            factor_group(f, g, G, 0);
-            int h_bad = 0;
-            CK(cudaMemcpyAsync(&h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-            sync(ctx);
-            if (h_bad != 0x7fffffff) {
-                const int k = f->kb + h_bad;
-                if (facts) *facts += h_bad;  // nodes factored before it (filterop.cpp:74-76)
-                char buf[256];
-                std::snprintf(buf, sizeof(buf),
-                              "factorize_node: singular factorization at node %d (z = %f+%fi)", k,
-                              f->zr[k], f->zi[k]);
-                Fail fl{FL_SINGULAR_NODE, buf};
-                fl.index = k;
-                fl.zr = f->zr[k];
-                fl.zi = f->zi[k];
-                throw fl;
+            const int nsr = std::min(ns, G);
+            for (int j = 0; j < nsr; ++j) {
+                const int c0 = (int)((long)G * j / nsr), c1 = (int)((long)G * (j + 1) / nsr);
+                const int s0 = (int)((long)slots * j / ns);
+                factor_group(f, g + c0, c1 - c0, s0, ctx->aux[j]);
+                solve_group(f, g + c0, c1 - c0, s0, X, ldx, P, ctx->aux[j]);
             }
-            solve_group(f, g, G, 0, X, ldx, P);
         }
         new_facts = f->nc;
     }
-    if (f->cache) {
+    for (int j = 0; j < ns; ++j) {
+        CK(cudaEventRecord(ctx->join[j], ctx->aux[j]));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->join[j], 0));
+    }
+    {
         int h_bad = 0;
         CK(cudaMemcpyAsync(&h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
         if (h_bad != 0x7fffffff) {
             const int k = f->kb + h_bad;
-            std::fill(f->factored.begin(), f->factored.end(), 0);
+            if (f->cache) std::fill(f->factored.begin(), f->factored.end(), 0);
+            else if (facts) *facts += h_bad;  // nodes factored before it (filterop.cpp:74-76)
             char buf[256];
             std::snprintf(buf, sizeof(buf),
                           "factorize_node: singular factorization at node %d (z = %f+%fi)", k,
@@ -437,18 +464,18 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             fl.zi = f->zi[k];
             throw fl;
         }
-        if (ctx->nranks > 1) {
-            // factorizations are counted globally: every rank adds the same total
-            long long loc = new_facts, tot = 0;
-            DBuf t;
-            t.ensure(sizeof(long long));
-            CK(cudaMemcpyAsync(t.p, &loc, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
-            nccl_check(ncclAllReduce(t.p, t.p, 1, ncclInt64, ncclSum, ctx->comm, ctx->stream),
-                       "ncclAllReduce(facts)");
-            CK(cudaMemcpyAsync(&tot, t.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
-            sync(ctx);
-            new_facts = tot;
-        }
+    }
+    if (f->cache && ctx->nranks > 1) {
+        // factorizations are counted globally: every rank adds the same total
+        long long loc = new_facts, tot = 0;
+        DBuf t;
+        t.ensure(sizeof(long long));
+        CK(cudaMemcpyAsync(t.p, &loc, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+        nccl_check(ncclAllReduce(t.p, t.p, 1, ncclInt64, ncclSum, ctx->comm, ctx->stream),
+                   "ncclAllReduce(facts)");
+        CK(cudaMemcpyAsync(&tot, t.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        new_facts = tot;
     }
     // ordered accumulation over the local nodes
     NodeShifts w{};
@@ -694,6 +721,14 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         c->device = device;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        const int naux = 4;
+        c->aux.resize(naux);
+        c->join.resize(naux);
+        for (int j = 0; j < naux; ++j) {
+            CK(cudaStreamCreateWithFlags(&c->aux[j], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->join[j], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         c->rank = rank;
         c->nranks = nranks;
         if (nranks > 1) {
@@ -730,6 +765,12 @@ int fl_ctx_destroy(fl_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (cudaStream_t a : ctx->aux) {
+        cudaStreamSynchronize(a);
+        cudaStreamDestroy(a);
+    }
+    for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return FL_OK;

@@ -80,8 +80,15 @@ __global__ void __launch_bounds__(128) dgemm_kernel(DGemm g) {
     }
 }
 
-// C -= A * B (planar complex). A: MxK "MK", B: KxN "KM".
-__global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
+// Planar complex tile update, A: MxK "MK", B: KxN "KM".
+//   SUB: C <- C - A B   (LU trailing update, solve updates). The C tile is
+//        loaded straight into the DMMA accumulators before the main loop, so
+//        its HBM latency overlaps the first operand tile's cp.async instead of
+//        serialising in the epilogue; A fragments are negated in registers.
+//   SET: C <- A B       (multiplication by the inverted 64x64 diagonal blocks;
+//        in place is safe: a CTA consumes its whole K range before storing).
+template <bool SUB>
+__global__ void __launch_bounds__(128) zgemm_kernel(ZGemm g) {
     extern __shared__ __align__(16) double smem[];
     // per stage: Ar, Ai, Br, Bi
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
@@ -95,12 +102,6 @@ __global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
     double* Cr = g.Cr + z * g.strideC;
     double* Ci = g.Ci + z * g.strideC;
 
-    double accr[4][4][2], acci[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
-
     auto issue = [&](int st, int kt) {
         double* base = smem + st * 4 * TILE_DOUBLES;
         load_tile<false>(base, tile_ptr<false>(Ar, g.lda, m0, kt * GK), g.lda, tid);
@@ -110,8 +111,27 @@ __global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
     };
 
     const int KT = g.K / GK;
-    issue(0, 0);
+    if (KT > 0) issue(0, 0);
     cp_async_commit();
+
+    double accr[4][4][2], acci[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (SUB) {
+                    const long off = (long)(n0 + wn + j * 8 + 2 * tq + e) * g.ldc + m0 + wm + i * 8 + gq;
+                    accr[i][j][e] = Cr[off];
+                    acci[i][j][e] = Ci[off];
+                } else {
+                    accr[i][j][e] = 0.0;
+                    acci[i][j][e] = 0.0;
+                }
+            }
+    constexpr double sgn = SUB ? -1.0 : 1.0;
+
     for (int kt = 0; kt < KT; ++kt) {
         cp_async_wait<0>();
         __syncthreads();
@@ -127,8 +147,8 @@ __global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
             double ar[4], ai[4], nai[4], br[4], bi[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                ar[i] = frag<false>(ar_s, wm + i * 8 + gq, kk + tq);
-                ai[i] = frag<false>(ai_s, wm + i * 8 + gq, kk + tq);
+                ar[i] = sgn * frag<false>(ar_s, wm + i * 8 + gq, kk + tq);
+                ai[i] = sgn * frag<false>(ai_s, wm + i * 8 + gq, kk + tq);
                 nai[i] = -ai[i];
             }
 #pragma unroll
@@ -156,8 +176,8 @@ __global__ void __launch_bounds__(128) zgemm_sub_kernel(ZGemm g) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const long off = (long)(n0 + wn + j * 8 + 2 * tq + e) * g.ldc + row;
-                Cr[off] -= accr[i][j][e];
-                Ci[off] -= acci[i][j][e];
+                Cr[off] = accr[i][j][e];
+                Ci[off] = acci[i][j][e];
             }
         }
     }
@@ -183,8 +203,16 @@ void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0 || batch <= 0) return;
     dim3 grid(g.M / GB, g.N / GB, batch);
     const size_t sm = 2 * 4 * TILE_DOUBLES * sizeof(double);
-    ensure_smem((const void*)zgemm_sub_kernel, sm);
-    zgemm_sub_kernel<<<grid, 128, sm, s>>>(g);
+    ensure_smem((const void*)zgemm_kernel<true>, sm);
+    zgemm_kernel<true><<<grid, 128, sm, s>>>(g);
+}
+
+void launch_zgemm_set(const ZGemm& g, int batch, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0 || batch <= 0) return;
+    dim3 grid(g.M / GB, g.N / GB, batch);
+    const size_t sm = 2 * 4 * TILE_DOUBLES * sizeof(double);
+    ensure_smem((const void*)zgemm_kernel<false>, sm);
+    zgemm_kernel<false><<<grid, 128, sm, s>>>(g);
 }
 
 }  // namespace fl

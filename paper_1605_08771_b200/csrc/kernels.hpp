@@ -26,6 +26,9 @@ struct ZGemm {
     double *Cr, *Ci; long ldc; long strideC;
 };
 void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s);
+// Planar complex C = A B (in place with B == C allowed: each CTA reads its
+// whole K range before storing).
+void launch_zgemm_set(const ZGemm& g, int batch, cudaStream_t s);
 
 // A planar-complex batch of N x N factor matrices: node b's planes start at
 // re + b*stride and im + b*stride, leading dimension ld (= N).
@@ -49,12 +52,11 @@ void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& 
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int batch, cudaStream_t s);
 // Apply the panel's 64 row interchanges to all columns outside the panel.
 void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cudaStream_t s);
-// B <- L^{-1} B for the unit-lower 64x64 block at (k0, k0); B = F[k0:k0+64, c0:c0+ncols].
-void launch_trsm_unit_lower(ZBatch L, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
-                            cudaStream_t s);
-// B <- U^{-1} B for the upper 64x64 block at (k0, k0).
-void launch_trsm_upper(ZBatch U, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
-                       cudaStream_t s);
+// Inverses of `nblocks` consecutive 64x64 diagonal blocks starting at (r0, r0):
+// unit-lower (upper=false) or upper. Block j of node b is stored at
+// Inv.re/im + b*Inv.stride + (first_block + j)*4096, column-major ld 64.
+void launch_trinv(ZBatch T, int r0, int nblocks, bool upper, ZBatch Inv, int first_block,
+                  int batch, cudaStream_t s);
 // perm[b*N + i] from the row interchanges ipiv (LAPACK-style sequence).
 void launch_ipiv_to_perm(const int* ipiv, int* perm, int N, int batch, cudaStream_t s);
 // W_b = complex(P_b X): Wr[i,c] = X[perm[i], c], Wi = 0 for c < P.

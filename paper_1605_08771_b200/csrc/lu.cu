@@ -271,55 +271,45 @@ void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cud
     laswp_panel_kernel<<<dim3((ncols + 127) / 128, batch), 128, 0, s>>>(F, N, k0, ipiv);
 }
 
-// ------------------------------------------------------------------ triangular 64x64 blocks
-// Strip of 32 RHS columns per CTA, 256 threads: thread (col = tid&31, q = tid>>5)
-// owns rows q, q+8, ..., q+56 of its column, in shared memory.
-constexpr int TS_COLS = 32;
-struct TriShared {
-    double Lr[PW][PW + 1];
-    double Li[PW][PW + 1];
-    double Xr[PW][TS_COLS + 1];
-    double Xi[PW][TS_COLS + 1];
+// ------------------------------------------------------------------ 64x64 triangular inverses
+// Inverse of the unit-lower (L) or upper (U) 64x64 diagonal block at (r0, r0)
+// of every node, by substitution on the identity in shared memory. The
+// triangular solves then become DMMA GEMMs (zgemm SET) with these blocks.
+// 256 threads: thread (col = tid & 63, q = tid >> 6) owns rows q, q+4, ...
+struct InvShared {
+    double Tr[PW][PW + 1];
+    double Ti[PW][PW + 1];
+    double Xr[PW][PW + 1];
+    double Xi[PW][PW + 1];
 };
 
 template <bool UPPER>
-__global__ void __launch_bounds__(256) trsm64_kernel(ZBatch T, int k0, ZBatch B, int brow0,
-                                                     int bcol0, int ncols) {
+__global__ void __launch_bounds__(256) trinv_kernel(ZBatch T, int r0, int blk_stride_nodes,
+                                                    ZBatch Inv, int first_block) {
     extern __shared__ __align__(16) unsigned char raw[];
-    TriShared& sh = *reinterpret_cast<TriShared*>(raw);
+    InvShared& sh = *reinterpret_cast<InvShared*>(raw);
     const int b = blockIdx.y;
+    const int blk = first_block + blockIdx.x;
+    const int k0 = r0 + blockIdx.x * PW;
     const double* Tr = T.re + b * T.stride;
     const double* Ti = T.im + b * T.stride;
-    double* Br = B.re + b * B.stride;
-    double* Bi = B.im + b * B.stride;
     const int tid = threadIdx.x;
-    const int c0 = blockIdx.x * TS_COLS;
-    // load the triangle (row i, col k) and the RHS strip
     for (int e = tid; e < PW * PW; e += 256) {
         const int i = e & (PW - 1), k = e >> 6;
         const long o = (long)(k0 + k) * T.ld + k0 + i;
-        sh.Lr[i][k] = Tr[o];
-        sh.Li[i][k] = Ti[o];
-    }
-    for (int e = tid; e < PW * TS_COLS; e += 256) {
-        const int i = e & (PW - 1), c = e >> 6;
-        if (c0 + c < ncols) {
-            const long o = (long)(bcol0 + c0 + c) * B.ld + brow0 + i;
-            sh.Xr[i][c] = Br[o];
-            sh.Xi[i][c] = Bi[o];
-        } else {
-            sh.Xr[i][c] = 0.0;
-            sh.Xi[i][c] = 0.0;
-        }
+        sh.Tr[i][k] = Tr[o];
+        sh.Ti[i][k] = Ti[o];
+        sh.Xr[i][k] = (i == k) ? 1.0 : 0.0;
+        sh.Xi[i][k] = 0.0;
     }
     __syncthreads();
-    const int col = tid & 31, q = tid >> 5;
+    const int col = tid & 63, q = tid >> 6;
     if (!UPPER) {
         for (int r = 0; r < PW - 1; ++r) {
             const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
-            for (int i = q; i < PW; i += 8) {
+            for (int i = q; i < PW; i += 4) {
                 if (i > r) {
-                    const cplx l{sh.Lr[i][r], sh.Li[i][r]};
+                    const cplx l{sh.Tr[i][r], sh.Ti[i][r]};
                     sh.Xr[i][col] -= l.re * x.re - l.im * x.im;
                     sh.Xi[i][col] -= l.re * x.im + l.im * x.re;
                 }
@@ -328,51 +318,43 @@ __global__ void __launch_bounds__(256) trsm64_kernel(ZBatch T, int k0, ZBatch B,
         }
     } else {
         for (int r = PW - 1; r >= 0; --r) {
-            if (q == (r & 7)) {
-                const cplx d{sh.Lr[r][r], sh.Li[r][r]};
-                const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
-                // x / d (complex division as std::complex does: x * conj(d) / |d|^2 scaled)
-                const cplx inv = crecip(d);
-                const cplx y = cmul(x, inv);
+            if (q == (r & 3)) {
+                const cplx inv = crecip(cplx{sh.Tr[r][r], sh.Ti[r][r]});
+                const cplx y = cmul(cplx{sh.Xr[r][col], sh.Xi[r][col]}, inv);
                 sh.Xr[r][col] = y.re;
                 sh.Xi[r][col] = y.im;
             }
             __syncthreads();
             const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
-            for (int i = q; i < r; i += 8) {
-                const cplx u{sh.Lr[i][r], sh.Li[i][r]};
+            for (int i = q; i < r; i += 4) {
+                const cplx u{sh.Tr[i][r], sh.Ti[i][r]};
                 sh.Xr[i][col] -= u.re * x.re - u.im * x.im;
                 sh.Xi[i][col] -= u.re * x.im + u.im * x.re;
             }
             __syncthreads();
         }
     }
-    for (int e = tid; e < PW * TS_COLS; e += 256) {
-        const int i = e & (PW - 1), c = e >> 6;
-        if (c0 + c < ncols) {
-            const long o = (long)(bcol0 + c0 + c) * B.ld + brow0 + i;
-            Br[o] = sh.Xr[i][c];
-            Bi[o] = sh.Xi[i][c];
-        }
+    double* Ir = Inv.re + b * Inv.stride + (long)blk * PW * PW;
+    double* Ii = Inv.im + b * Inv.stride + (long)blk * PW * PW;
+    for (int e = tid; e < PW * PW; e += 256) {
+        const int i = e & (PW - 1), k = e >> 6;
+        Ir[(long)k * PW + i] = sh.Xr[i][k];
+        Ii[(long)k * PW + i] = sh.Xi[i][k];
     }
+    (void)blk_stride_nodes;
 }
 
-void launch_trsm_unit_lower(ZBatch L, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
-                            cudaStream_t s) {
-    if (ncols <= 0) return;
-    const size_t sm = sizeof(TriShared);
-    ensure_smem((const void*)trsm64_kernel<false>, sm);
-    trsm64_kernel<false><<<dim3((ncols + TS_COLS - 1) / TS_COLS, batch), 256, sm, s>>>(
-        L, k0, B, brow0, bcol0, ncols);
-}
-
-void launch_trsm_upper(ZBatch U, int k0, ZBatch B, int brow0, int bcol0, int ncols, int batch,
-                       cudaStream_t s) {
-    if (ncols <= 0) return;
-    const size_t sm = sizeof(TriShared);
-    ensure_smem((const void*)trsm64_kernel<true>, sm);
-    trsm64_kernel<true><<<dim3((ncols + TS_COLS - 1) / TS_COLS, batch), 256, sm, s>>>(
-        U, k0, B, brow0, bcol0, ncols);
+void launch_trinv(ZBatch T, int r0, int nblocks, bool upper, ZBatch Inv, int first_block,
+                  int batch, cudaStream_t s) {
+    if (nblocks <= 0) return;
+    const size_t sm = sizeof(InvShared);
+    if (upper) {
+        ensure_smem((const void*)trinv_kernel<true>, sm);
+        trinv_kernel<true><<<dim3(nblocks, batch), 256, sm, s>>>(T, r0, 0, Inv, first_block);
+    } else {
+        ensure_smem((const void*)trinv_kernel<false>, sm);
+        trinv_kernel<false><<<dim3(nblocks, batch), 256, sm, s>>>(T, r0, 0, Inv, first_block);
+    }
 }
 
 // ------------------------------------------------------------------ pivots -> permutation
