@@ -248,7 +248,6 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    ctx.set_profiling(True)
     l0 = ctx.launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -259,9 +258,20 @@ def run_b200(args, rank, world, local_rank):
     e1.synchronize()
     launches = ctx.launches() - l0
     ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    # per-kernel-class CUDA events over K more steps with the node chunks
+    # serialised (1 stream), so each class's event time is its own
+    ctx.set_streams(1)
+    ctx.set_profiling(True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms_serial = e0.elapsed_time(e1)
     prof = {k: ctx.profile(k) for k in P.Context.KERNEL_CLASSES}
     ctx.set_profiling(False)
-    clk = clocks.stop()
+    ctx.set_streams(4)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -332,15 +342,18 @@ def run_b200(args, rank, world, local_rank):
                    "parallelism": f"contour nodes sharded {nc}/{world} per GPU + NCCL allreduce",
                    "l2": "inputs larger than L2 (n_c LU factors, 16 n^2 B each)"},
         "fraction_of_fp64_peak": round(value / 1e3 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
-        "roofline": {"kernel": "zgemm_sub_kernel (LU trailing update + blocked solves)",
+        "roofline": {"kernel": "zgemm_kernel (DMMA; LU trailing update, U12 and blocked solves)",
                      "bound": "tensor", "achieved": round(achieved, 3),
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": None,
                      "peak_source": "measured FP64 DMMA burst, tools/fp64_peak.cu "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
-                     "share_of_step": round(zms / total_ms_prof, 4) if total_ms_prof else None,
-                     "launches": zl},
+                     "share_of_step": round(zms / ms_serial, 4) if ms_serial else None,
+                     "launches_per_step": zl / args.steps,
+                     "timing": "CUDA events per launch, node chunks serialised (1 stream) "
+                               "over K extra steps"},
+        "serial_ms_per_step": round(ms_serial / args.steps, 3),
         "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 3),
                         "work_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
                     for k, v in prof.items()},

@@ -81,6 +81,8 @@ long long fl_ctx_launches(const fl_ctx* ctx);
    classes "shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
    "allreduce"; work = algorithmic flops (GEMM/TRSM) or bytes (streams). */
 int fl_ctx_set_profiling(fl_ctx* ctx, int on);
+/* number of contour-node chunks factored/solved concurrently (1..4, default 4) */
+int fl_ctx_set_streams(fl_ctx* ctx, int n);
 int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,
                    fl_err* err);
 

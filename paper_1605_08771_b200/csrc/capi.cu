@@ -133,6 +133,7 @@ struct fl_ctx {
     std::vector<cudaStream_t> aux;  // node-chunk streams (fork/join on `stream`)
     cudaEvent_t fork = nullptr;
     std::vector<cudaEvent_t> join;
+    int nstreams = 4;  // node chunks in flight (<= aux.size())
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
         scal;
@@ -163,7 +164,7 @@ struct fl_filter {
     bool cache;
     int kb = 0, ke = 0;  // local node range [kb, ke)
     // factors: cache -> one per local node; else a rotating group
-    DBuf fac_re, fac_im, ipiv, perm, bad;
+    DBuf fac_re, fac_im, ipiv, perm, bad, ptab;
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     int fac_slots = 0;
     std::vector<char> factored;  // cache mode, per local node
@@ -264,6 +265,7 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
         z.zi[b] = f->zi[f->kb + g0 + b];
     }
     int* ipiv = f->ipiv.i() + (long)s0 * N;
+    int* ptab = f->ptab.i() + (long)s0 * (4 * FL_TILE + 1);
     const int NB = N / FL_TILE;
     const long istride = 2L * NB * FL_TILE * FL_TILE;
     ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
@@ -274,12 +276,12 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
     for (int k0 = 0; k0 < N; k0 += FL_TILE) {
         {
             Prof pr(ctx, P_PANEL, 0.0, 2, st);
-            launch_panel(F, N, k0, ipiv, G, st);
+            launch_panel(F, N, k0, ipiv, ptab, G, st);
             launch_trinv(F, k0, 1, false, Inv, k0 / FL_TILE, G, st);
         }
         {
             Prof pr(ctx, P_LASWP, 0.0, 1, st);
-            launch_laswp_panel(F, N, k0, ipiv, G, st);
+            launch_laswp_panel(F, N, k0, ptab, G, st);
         }
         const int rest = N - k0 - FL_TILE;
         if (rest > 0) {
@@ -398,6 +400,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->fac_im.ensure(sizeof(double) * (size_t)fstride * slots);
         f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
         f->perm.ensure(sizeof(int) * (size_t)N * slots);
+        f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * slots);
         f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->fac_slots = slots;
@@ -408,7 +411,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     CK(cudaMemcpyAsync(f->bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     // Node chunks run concurrently on the context's auxiliary streams so one
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
-    const int ns = std::max(1, std::min<int>(std::min(L, slots), (int)ctx->aux.size()));
+    const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
     CK(cudaEventRecord(ctx->fork, ctx->stream));
     for (int j = 0; j < ns; ++j) CK(cudaStreamWaitEvent(ctx->aux[j], ctx->fork, 0));
     long long new_facts = 0;
@@ -792,6 +795,12 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 }
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
+
+int fl_ctx_set_streams(fl_ctx* ctx, int n) {
+    CtxLock lk(ctx);
+    ctx->nstreams = std::max(1, std::min(n, (int)ctx->aux.size()));
+    return FL_OK;
+}
 
 int fl_ctx_set_profiling(fl_ctx* ctx, int on) {
     CtxLock lk(ctx);

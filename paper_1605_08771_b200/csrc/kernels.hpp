@@ -48,10 +48,11 @@ struct NodeShifts {
 // F_b = z_b I - A (A real N x N, zero-padded beyond n).
 void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& z, int batch,
                   cudaStream_t s);
-// Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j].
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int batch, cudaStream_t s);
-// Apply the panel's 64 row interchanges to all columns outside the panel.
-void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cudaStream_t s);
+// Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j];
+// ptab[b*257 ...] receives the panel's net row permutation (count, rows, sources).
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s);
+// Apply the panel's 64 row interchanges (ptab) to all columns outside the panel.
+void launch_laswp_panel(ZBatch F, int N, int k0, const int* ptab, int batch, cudaStream_t s);
 // Inverses of `nblocks` consecutive 64x64 diagonal blocks starting at (r0, r0):
 // unit-lower (upper=false) or upper. Block j of node b is stored at
 // Inv.re/im + b*Inv.stride + (first_block + j)*4096, column-major ld 64.

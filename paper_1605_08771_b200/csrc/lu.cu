@@ -86,10 +86,13 @@ struct PanelShared {
     int red_i[PTH / 32];
     int piv;
     int winner;
+    int pivs[PW];       // this panel's pivot rows (rank 0)
+    int tpos[2 * PW];   // net row permutation of the panel: row tpos[m] <- row tsrc[m]
+    int tsrc[2 * PW];
 };
 
 __global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
-    panel_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv) {
+    panel_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ PanelShared sh;
     const int rank = (int)cluster.block_rank();
@@ -200,7 +203,10 @@ __global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
             sh.u[0][tid] = ur;
             sh.u[1][tid] = ui;
         }
-        if (rank == 0 && tid == 0) ipiv[(long)b * N + j] = piv;
+        if (rank == 0 && tid == 0) {
+            ipiv[(long)b * N + j] = piv;
+            sh.pivs[jj] = piv;
+        }
         __syncthreads();
         // scale column j, rank-1 update of columns j+1..k0+63, candidates for j+1
         const cplx pv{sh.u[0][jj], sh.u[1][jj]};
@@ -215,16 +221,28 @@ __global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
                 Fr[at(r, j)] = l.re;
                 Fi[at(r, j)] = l.im;
             }
-            for (int c = jj + 1; c < PW; ++c) {
-                const long o = at(r, k0 + c);
-                const double ur = sh.u[0][c], ui = sh.u[1][c];
-                double xr = Fr[o], xi = Fi[o];
-                xr -= l.re * ur - l.im * ui;
-                xi -= l.re * ui + l.im * ur;
-                Fr[o] = xr;
-                Fi[o] = xi;
-                if (c == jj + 1) {
-                    double sc = xr * xr + xi * xi;
+            // chunks of 8 columns: all loads of a chunk are issued before any
+            // store so the L2 round trips overlap (stores would otherwise
+            // order every following load behind them)
+            for (int c0 = jj + 1; c0 < PW; c0 += 8) {
+                double xr[8], xi[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (c0 + k < PW) {
+                        xr[k] = Fr[at(r, k0 + c0 + k)];
+                        xi[k] = Fi[at(r, k0 + c0 + k)];
+                    }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (c0 + k < PW) {
+                        const double ur = sh.u[0][c0 + k], ui = sh.u[1][c0 + k];
+                        xr[k] -= l.re * ur - l.im * ui;
+                        xi[k] -= l.re * ui + l.im * ur;
+                        Fr[at(r, k0 + c0 + k)] = xr[k];
+                        Fi[at(r, k0 + c0 + k)] = xi[k];
+                    }
+                if (c0 == jj + 1) {
+                    const double sc = xr[0] * xr[0] + xi[0] * xi[0];
                     if (better(sc, r, s, idx)) { s = sc; idx = r; }
                 }
             }
@@ -235,40 +253,106 @@ __global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
             publish(j + 1, par ^ 1, s, idx);
         }
     }
+    // rank 0: net permutation of the 64 interchanges (<= 128 rows move) for laswp
+    if (rank == 0 && wid == 0) {
+        for (int m = lane; m < PW; m += 32) {
+            sh.tpos[m] = k0 + m;
+            sh.tsrc[m] = k0 + m;
+        }
+        int cnt = PW;
+        __syncwarp();
+        for (int q = 0; q < PW; ++q) {
+            const int pr = sh.pivs[q];
+            if (pr == k0 + q) continue;
+            int at_p;
+            if (pr < k0 + PW) {
+                at_p = pr - k0;
+            } else {
+                int hit = -1;
+                for (int base = PW; base < cnt; base += 32) {
+                    const int m = base + lane;
+                    const unsigned bal = __ballot_sync(0xffffffffu, m < cnt && sh.tpos[m] == pr);
+                    if (bal && hit < 0) hit = base + __ffs(bal) - 1;
+                }
+                if (hit < 0) {
+                    hit = cnt;
+                    if (lane == 0) {
+                        sh.tpos[cnt] = pr;
+                        sh.tsrc[cnt] = pr;
+                    }
+                    ++cnt;
+                }
+                at_p = hit;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int t = sh.tsrc[q];
+                sh.tsrc[q] = sh.tsrc[at_p];
+                sh.tsrc[at_p] = t;
+            }
+            __syncwarp();
+        }
+        int* tab = ptab + (long)b * (4 * PW + 1);
+        if (lane == 0) tab[0] = cnt;
+        for (int m = lane; m < cnt; m += 32) {
+            tab[1 + m] = sh.tpos[m];
+            tab[1 + 2 * PW + m] = sh.tsrc[m];
+        }
+    }
     cluster.sync();  // keep shared memory alive until every CTA is done reading it
 }
 
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int batch, cudaStream_t s) {
-    panel_kernel<<<dim3(PCL, batch), PTH, 0, s>>>(F, N, k0, ipiv);
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+    panel_kernel<<<dim3(PCL, batch), PTH, 0, s>>>(F, N, k0, ipiv, ptab);
 }
 
 // ------------------------------------------------------------------ laswp
-// One thread per column outside the panel; the 64 interchanges in order.
-__global__ void laswp_panel_kernel(ZBatch F, int N, int k0, const int* __restrict__ ipiv) {
+// The panel's 64 interchanges applied to the columns outside the panel as one
+// gather/scatter of the <= 128 moved rows (net permutation from the panel
+// kernel): every load of a CTA is issued before any store.
+constexpr int LS_COLS = 16;
+__global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int N, int k0,
+                                                          const int* __restrict__ ptab) {
+    __shared__ double vr[2 * PW][LS_COLS + 1];
+    __shared__ double vi[2 * PW][LS_COLS + 1];
+    __shared__ int pos[2 * PW], src[2 * PW];
     const int b = blockIdx.y;
-    int col = blockIdx.x * blockDim.x + threadIdx.x;
+    const int* tab = ptab + (long)b * (4 * PW + 1);
+    const int cnt = tab[0];
+    for (int m = threadIdx.x; m < cnt; m += blockDim.x) {
+        pos[m] = tab[1 + m];
+        src[m] = tab[1 + 2 * PW + m];
+    }
+    __syncthreads();
     const int ncols = N - PW;
-    if (col >= ncols) return;
-    if (col >= k0) col += PW;
-    double* Fr = F.re + b * F.stride + (long)col * F.ld;
-    double* Fi = F.im + b * F.stride + (long)col * F.ld;
-    const int* ip = ipiv + (long)b * N;
-    for (int j = k0; j < k0 + PW; ++j) {
-        const int p = ip[j];
-        if (p != j) {
-            double tr = Fr[j], ti = Fi[j];
-            Fr[j] = Fr[p];
-            Fi[j] = Fi[p];
-            Fr[p] = tr;
-            Fi[p] = ti;
-        }
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    const int c0 = blockIdx.x * LS_COLS;
+    for (int e = threadIdx.x; e < cnt * LS_COLS; e += blockDim.x) {
+        const int m = e % cnt, c = e / cnt;
+        int col = c0 + c;
+        if (col >= ncols) continue;
+        if (col >= k0) col += PW;
+        const long o = (long)col * F.ld + src[m];
+        vr[m][c] = Fr[o];
+        vi[m][c] = Fi[o];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * LS_COLS; e += blockDim.x) {
+        const int m = e % cnt, c = e / cnt;
+        int col = c0 + c;
+        if (col >= ncols) continue;
+        if (col >= k0) col += PW;
+        const long o = (long)col * F.ld + pos[m];
+        Fr[o] = vr[m][c];
+        Fi[o] = vi[m][c];
     }
 }
 
-void launch_laswp_panel(ZBatch F, int N, int k0, const int* ipiv, int batch, cudaStream_t s) {
+void launch_laswp_panel(ZBatch F, int N, int k0, const int* ptab, int batch, cudaStream_t s) {
     const int ncols = N - PW;
     if (ncols <= 0) return;
-    laswp_panel_kernel<<<dim3((ncols + 127) / 128, batch), 128, 0, s>>>(F, N, k0, ipiv);
+    laswp_panel_kernel<<<dim3((ncols + LS_COLS - 1) / LS_COLS, batch), 256, 0, s>>>(F, N, k0, ptab);
 }
 
 // ------------------------------------------------------------------ 64x64 triangular inverses

@@ -112,6 +112,10 @@ class Context:
     KERNEL_CLASSES = ("shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
                       "allreduce")
 
+    def set_streams(self, n: int) -> None:
+        """Contour-node chunks in flight (1 serialises the filter's kernels)."""
+        L.lib().fl_ctx_set_streams(self.handle, int(n))
+
     def set_profiling(self, on: bool) -> None:
         """Per-kernel-class CUDA-event timing on the context stream."""
         L.lib().fl_ctx_set_profiling(self.handle, int(bool(on)))
