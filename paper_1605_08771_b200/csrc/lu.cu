@@ -2,11 +2,11 @@
 // (NodeFactorization, proj/src/filterop.cpp:9-32), batched over contour nodes.
 //
 //  shift        F = z I - A                          HBM stream, 24 N^2 B / node
-//  panel        64-wide panel, partial pivoting      8-CTA cluster, DSMEM pivot
-//                                                    exchange, 1 cluster barrier / column
-//  laswp        row interchanges outside the panel
-//  trsm         64x64 triangular blocks (unit-lower / upper) on a column strip
-//  zgemm_sub    trailing update / solve updates      DMMA (gemm.cu)
+//  panel        64-wide panel, partial pivoting      panel.cu (8-CTA cluster,
+//                                                    register-resident leaves)
+//  laswp        row interchanges outside the panel   one gather/scatter per panel
+//  trinv        64x64 diagonal-block inverses        triangular solves become GEMMs
+//  zgemm        trailing update / solve updates      DMMA (gemm.cu)
 #include <cooperative_groups.h>
 
 #include <mutex>
@@ -62,249 +62,8 @@ void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& 
 }
 
 // ------------------------------------------------------------------ panel
-// Cluster of PCL CTAs per node. CTA r owns panel rows [k0 + r*R, k0 + (r+1)*R).
-// Per column j (one cluster barrier):
-//   every CTA published (score, row) of its best candidate for column j plus a
-//   copy of that candidate row's 64 panel entries, and the owner of row j a
-//   copy of row j (double-buffered by j parity) -> after the barrier each CTA
-//   reduces the PCL candidates (ties -> lowest row, Eigen's maxCoeff), takes the
-//   pivot row from the winner's shared memory (DSMEM) and the owners of rows j
-//   and piv write the interchanged rows; then each CTA scales its rows of
-//   column j and applies the rank-1 update to the panel columns right of j,
-//   fusing the candidate search for column j+1.
-constexpr int PCL = 8;
-constexpr int PTH = 512;
+// panel.cu: register-resident two-level cluster panel (launch_panel).
 constexpr int PW = 64;
-
-struct PanelShared {
-    double cand_score[2];
-    int cand_row[2];
-    double cand_vals[2][2][PW];  // [parity][re/im][col]
-    double diag_vals[2][2][PW];
-    double u[2][PW];             // pivot row (this column)
-    double red_s[PTH / 32];
-    int red_i[PTH / 32];
-    int piv;
-    int winner;
-    int pivs[PW];       // this panel's pivot rows (rank 0)
-    int tpos[2 * PW];   // net row permutation of the panel: row tpos[m] <- row tsrc[m]
-    int tsrc[2 * PW];
-};
-
-__global__ void __cluster_dims__(PCL, 1, 1) __launch_bounds__(PTH)
-    panel_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
-    cg::cluster_group cluster = cg::this_cluster();
-    __shared__ PanelShared sh;
-    const int rank = (int)cluster.block_rank();
-    const int b = blockIdx.y;
-    double* Fr = F.re + b * F.stride;
-    double* Fi = F.im + b * F.stride;
-    const long ld = F.ld;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int rows_total = N - k0;
-    const int R = (rows_total + PCL - 1) / PCL;
-    const int lo = k0 + rank * R;
-    const int hi = min(N, lo + R);
-
-    auto at = [&](int r, int c) { return (long)c * ld + r; };
-
-    // candidate search for column c over own rows >= rmin, then publish
-    auto publish = [&](int c, int par, double s, int idx) {
-        warp_argmax(s, idx);
-        if (lane == 0) { sh.red_s[wid] = s; sh.red_i[wid] = idx; }
-        __syncthreads();
-        if (wid == 0) {
-            double s2 = lane < PTH / 32 ? sh.red_s[lane] : -1.0;
-            int i2 = lane < PTH / 32 ? sh.red_i[lane] : 0x7fffffff;
-            warp_argmax(s2, i2);
-            if (lane == 0) { sh.cand_score[par] = s2; sh.cand_row[par] = i2; }
-        }
-        __syncthreads();
-        const int cr = sh.cand_row[par];
-        if (tid < PW) {
-            if (cr >= 0 && cr < N) {
-                sh.cand_vals[par][0][tid] = Fr[at(cr, k0 + tid)];
-                sh.cand_vals[par][1][tid] = Fi[at(cr, k0 + tid)];
-            }
-            if (c >= lo && c < hi) {
-                sh.diag_vals[par][0][tid] = Fr[at(c, k0 + tid)];
-                sh.diag_vals[par][1][tid] = Fi[at(c, k0 + tid)];
-            }
-        }
-    };
-
-    // initial candidates for column k0
-    {
-        double s = -1.0;
-        int idx = 0x7fffffff;
-        for (int r = max(lo, k0) + tid; r < hi; r += PTH) {
-            double re = Fr[at(r, k0)], im = Fi[at(r, k0)];
-            double sc = re * re + im * im;
-            if (better(sc, r, s, idx)) { s = sc; idx = r; }
-        }
-        if (lo >= hi) idx = -1;
-        publish(k0, 0, s, idx);
-    }
-
-    for (int jj = 0; jj < PW; ++jj) {
-        const int j = k0 + jj;
-        const int par = jj & 1;
-        cluster.sync();
-        if (wid == 0) {
-            double s = -1.0;
-            int idx = 0x7fffffff, win = 0;
-            if (lane < PCL) {
-                PanelShared* rs = cluster.map_shared_rank(&sh, lane);
-                s = rs->cand_score[par];
-                idx = rs->cand_row[par];
-                if (idx < 0) { s = -1.0; idx = 0x7fffffff; }
-            }
-            int myrank = lane;
-            // argmax carrying the owning rank
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                double so = __shfl_xor_sync(0xffffffffu, s, off);
-                int io = __shfl_xor_sync(0xffffffffu, idx, off);
-                int ro = __shfl_xor_sync(0xffffffffu, myrank, off);
-                if (better(so, io, s, idx)) { s = so; idx = io; myrank = ro; }
-            }
-            win = myrank;
-            if (lane == 0) {
-                // all-zero column: Eigen keeps the diagonal row (no interchange)
-                if (!(s > 0.0)) idx = j;
-                sh.piv = idx;
-                sh.winner = win;
-            }
-        }
-        __syncthreads();
-        const int piv = sh.piv;
-        const int diag_owner = (j - k0) / R;
-        if (tid < PW) {
-            double ur, ui;
-            if (piv == j) {
-                PanelShared* ds = cluster.map_shared_rank(&sh, diag_owner);
-                ur = ds->diag_vals[par][0][tid];
-                ui = ds->diag_vals[par][1][tid];
-            } else {
-                PanelShared* ws = cluster.map_shared_rank(&sh, sh.winner);
-                ur = ws->cand_vals[par][0][tid];
-                ui = ws->cand_vals[par][1][tid];
-                if (piv >= lo && piv < hi) {
-                    // row piv receives the old row j
-                    PanelShared* ds = cluster.map_shared_rank(&sh, diag_owner);
-                    Fr[at(piv, k0 + tid)] = ds->diag_vals[par][0][tid];
-                    Fi[at(piv, k0 + tid)] = ds->diag_vals[par][1][tid];
-                }
-                if (j >= lo && j < hi) {
-                    Fr[at(j, k0 + tid)] = ur;
-                    Fi[at(j, k0 + tid)] = ui;
-                }
-            }
-            sh.u[0][tid] = ur;
-            sh.u[1][tid] = ui;
-        }
-        if (rank == 0 && tid == 0) {
-            ipiv[(long)b * N + j] = piv;
-            sh.pivs[jj] = piv;
-        }
-        __syncthreads();
-        // scale column j, rank-1 update of columns j+1..k0+63, candidates for j+1
-        const cplx pv{sh.u[0][jj], sh.u[1][jj]};
-        const bool nonzero = (pv.re != 0.0 || pv.im != 0.0);
-        const cplx inv = nonzero ? crecip(pv) : cplx{0.0, 0.0};
-        double s = -1.0;
-        int idx = 0x7fffffff;
-        for (int r = max(lo, j + 1) + tid; r < hi; r += PTH) {
-            cplx l{Fr[at(r, j)], Fi[at(r, j)]};
-            if (nonzero) {
-                l = cmul(l, inv);
-                Fr[at(r, j)] = l.re;
-                Fi[at(r, j)] = l.im;
-            }
-            // chunks of 8 columns: all loads of a chunk are issued before any
-            // store so the L2 round trips overlap (stores would otherwise
-            // order every following load behind them)
-            for (int c0 = jj + 1; c0 < PW; c0 += 8) {
-                double xr[8], xi[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (c0 + k < PW) {
-                        xr[k] = Fr[at(r, k0 + c0 + k)];
-                        xi[k] = Fi[at(r, k0 + c0 + k)];
-                    }
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (c0 + k < PW) {
-                        const double ur = sh.u[0][c0 + k], ui = sh.u[1][c0 + k];
-                        xr[k] -= l.re * ur - l.im * ui;
-                        xi[k] -= l.re * ui + l.im * ur;
-                        Fr[at(r, k0 + c0 + k)] = xr[k];
-                        Fi[at(r, k0 + c0 + k)] = xi[k];
-                    }
-                if (c0 == jj + 1) {
-                    const double sc = xr[0] * xr[0] + xi[0] * xi[0];
-                    if (better(sc, r, s, idx)) { s = sc; idx = r; }
-                }
-            }
-        }
-        if (jj + 1 < PW) {
-            if (max(lo, j + 1) >= hi) idx = -1;
-            __syncthreads();
-            publish(j + 1, par ^ 1, s, idx);
-        }
-    }
-    // rank 0: net permutation of the 64 interchanges (<= 128 rows move) for laswp
-    if (rank == 0 && wid == 0) {
-        for (int m = lane; m < PW; m += 32) {
-            sh.tpos[m] = k0 + m;
-            sh.tsrc[m] = k0 + m;
-        }
-        int cnt = PW;
-        __syncwarp();
-        for (int q = 0; q < PW; ++q) {
-            const int pr = sh.pivs[q];
-            if (pr == k0 + q) continue;
-            int at_p;
-            if (pr < k0 + PW) {
-                at_p = pr - k0;
-            } else {
-                int hit = -1;
-                for (int base = PW; base < cnt; base += 32) {
-                    const int m = base + lane;
-                    const unsigned bal = __ballot_sync(0xffffffffu, m < cnt && sh.tpos[m] == pr);
-                    if (bal && hit < 0) hit = base + __ffs(bal) - 1;
-                }
-                if (hit < 0) {
-                    hit = cnt;
-                    if (lane == 0) {
-                        sh.tpos[cnt] = pr;
-                        sh.tsrc[cnt] = pr;
-                    }
-                    ++cnt;
-                }
-                at_p = hit;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                const int t = sh.tsrc[q];
-                sh.tsrc[q] = sh.tsrc[at_p];
-                sh.tsrc[at_p] = t;
-            }
-            __syncwarp();
-        }
-        int* tab = ptab + (long)b * (4 * PW + 1);
-        if (lane == 0) tab[0] = cnt;
-        for (int m = lane; m < cnt; m += 32) {
-            tab[1 + m] = sh.tpos[m];
-            tab[1 + 2 * PW + m] = sh.tsrc[m];
-        }
-    }
-    cluster.sync();  // keep shared memory alive until every CTA is done reading it
-}
-
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
-    panel_kernel<<<dim3(PCL, batch), PTH, 0, s>>>(F, N, k0, ipiv, ptab);
-}
 
 // ------------------------------------------------------------------ laswp
 // The panel's 64 interchanges applied to the columns outside the panel as one

@@ -1,0 +1,409 @@
+// 64-wide LU panel with partial pivoting (Eigen PartialPivLU's unblocked_lu
+// semantics: pivot = argmax |a_ij| over rows >= j, lowest row on ties) for a
+// batch of contour nodes — one 8-CTA thread-block cluster per node.
+//
+// Two-level blocking inside the panel: the 64 columns are factored as 64/W
+// leaves of W columns. A leaf lives in REGISTERS (each thread owns ROWS panel
+// rows x W complex entries), so the column steps touch no memory at all:
+//   per column: block argmax of |x|^2 -> publish (score, row, the candidate's
+//   W entries) in shared memory -> ONE cluster barrier -> every CTA reduces the
+//   8 candidates through DSMEM, takes the pivot row from the winner's shared
+//   memory; the owners of rows j and piv exchange rows in registers; scale +
+//   rank-1 update in registers, fused with the next column's candidate search.
+// Between leaves: rank 0 applies the leaf's interchanges to the panel's other
+// columns as one gather/scatter of the moved rows, every CTA forms the leaf's
+// U block (L_qq^{-1} T, W x (remaining panel columns)) redundantly in shared
+// memory, and updates its own rows' remaining panel columns with its register
+// L entries (one global read-modify-write per row).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace fl {
+
+namespace {
+
+constexpr int PCL2 = 8;   // cluster size (portable)
+constexpr int PWID = 64;  // outer panel width
+
+template <int W>
+struct RegPanelShared {
+    double cand_score[2];
+    int cand_row[2];
+    double cand_vals[2][2][W];
+    double diag_vals[2][2][W];
+    double ur[W], ui[W];    // pivot row (this column)
+    double ojr[W], oji[W];  // old row j (goes to row piv)
+    double red_s[32];
+    int red_i[32];
+    int piv, winner;
+    int pivs[PWID];
+    // leaf U block: Lqq (W x W) and U (W x PWID)
+    double lr[W][W + 1], li[W][W + 1];
+    double Ur[W][PWID + 1], Ui[W][PWID + 1];
+    // row permutation scratch (rank 0)
+    int tpos[2 * PWID], tsrc[2 * PWID];
+    double gr[2 * W][PWID], gi[2 * W][PWID];
+};
+
+// net permutation of interchanges (first+q, piv[q]) q < count, by one warp;
+// returns the number of moved rows (rows tpos[m] <- tsrc[m])
+template <class SH>
+__device__ int net_permutation(SH& sh, int first, const int* piv, int count, int lane) {
+    for (int m = lane; m < count; m += 32) {
+        sh.tpos[m] = first + m;
+        sh.tsrc[m] = first + m;
+    }
+    int cnt = count;
+    __syncwarp();
+    for (int q = 0; q < count; ++q) {
+        const int pr = piv[q];
+        if (pr == first + q) continue;
+        int at_p;
+        if (pr < first + count) {
+            at_p = pr - first;
+        } else {
+            int hit = -1;
+            for (int base = count; base < cnt; base += 32) {
+                const int m = base + lane;
+                const unsigned bal = __ballot_sync(0xffffffffu, m < cnt && sh.tpos[m] == pr);
+                if (bal && hit < 0) hit = base + __ffs(bal) - 1;
+            }
+            if (hit < 0) {
+                hit = cnt;
+                if (lane == 0) {
+                    sh.tpos[cnt] = pr;
+                    sh.tsrc[cnt] = pr;
+                }
+                ++cnt;
+            }
+            at_p = hit;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int t = sh.tsrc[q];
+            sh.tsrc[q] = sh.tsrc[at_p];
+            sh.tsrc[at_p] = t;
+        }
+        __syncwarp();
+    }
+    return cnt;
+}
+
+}  // namespace
+
+template <int W, int ROWS, int NT>
+__global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
+    panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char raw[];
+    RegPanelShared<W>& sh = *reinterpret_cast<RegPanelShared<W>*>(raw);
+    const int rank = (int)cluster.block_rank();
+    const int b = blockIdx.y;
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    const long ld = F.ld;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = NT / 32;
+    const int R = (N - k0 + PCL2 - 1) / PCL2;  // rows per CTA (<= ROWS * NT)
+    const int base = k0 + rank * R;
+    const int top = min(N, base + R);
+    auto at = [&](int r, int c) { return (long)c * ld + r; };
+    auto owner_rank = [&](int r) { return (r - k0) / R; };
+
+    int row[ROWS];
+    bool has[ROWS];
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+        row[i] = base + tid + i * NT;
+        has[i] = row[i] < top;
+    }
+    double xr[ROWS][W], xi[ROWS][W];
+
+    for (int q = 0; q < PWID / W; ++q) {
+        const int c0 = k0 + q * W;
+        // ---- load the leaf (rows >= c0 of this CTA)
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+                if (has[i] && row[i] >= c0) {
+                    xr[i][k] = Fr[at(row[i], c0 + k)];
+                    xi[i][k] = Fi[at(row[i], c0 + k)];
+                } else {
+                    xr[i][k] = 0.0;
+                    xi[i][k] = 0.0;
+                }
+        // ---- column steps
+#pragma unroll
+        for (int jj = 0; jj < W; ++jj) {
+            const int j = c0 + jj;
+            const int par = j & 1;
+            // local candidate for column j over own rows >= j
+            double s = -1.0;
+            int idx = 0x7fffffff;
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i)
+                if (has[i] && row[i] >= j) {
+                    const double sc = xr[i][jj] * xr[i][jj] + xi[i][jj] * xi[i][jj];
+                    if (better(sc, row[i], s, idx)) {
+                        s = sc;
+                        idx = row[i];
+                    }
+                }
+            warp_argmax(s, idx);
+            if (lane == 0) {
+                sh.red_s[wid] = s;
+                sh.red_i[wid] = idx;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                double s2 = lane < NW ? sh.red_s[lane] : -1.0;
+                int i2 = lane < NW ? sh.red_i[lane] : 0x7fffffff;
+                warp_argmax(s2, i2);
+                if (lane == 0) {
+                    sh.cand_score[par] = s2;
+                    sh.cand_row[par] = (s2 >= 0.0) ? i2 : -1;
+                }
+            }
+            __syncthreads();
+            {
+                const int cr = sh.cand_row[par];
+#pragma unroll
+                for (int i = 0; i < ROWS; ++i) {
+                    if (has[i] && row[i] == cr)
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            sh.cand_vals[par][0][k] = xr[i][k];
+                            sh.cand_vals[par][1][k] = xi[i][k];
+                        }
+                    if (has[i] && row[i] == j)
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            sh.diag_vals[par][0][k] = xr[i][k];
+                            sh.diag_vals[par][1][k] = xi[i][k];
+                        }
+                }
+            }
+            cluster.sync();
+            if (wid == 0) {
+                double s2 = -1.0;
+                int i2 = 0x7fffffff, rk = lane;
+                if (lane < PCL2) {
+                    RegPanelShared<W>* rs = cluster.map_shared_rank(&sh, lane);
+                    s2 = rs->cand_score[par];
+                    i2 = rs->cand_row[par];
+                    if (i2 < 0) {
+                        s2 = -1.0;
+                        i2 = 0x7fffffff;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double so = __shfl_xor_sync(0xffffffffu, s2, off);
+                    const int io = __shfl_xor_sync(0xffffffffu, i2, off);
+                    const int ro = __shfl_xor_sync(0xffffffffu, rk, off);
+                    if (better(so, io, s2, i2)) {
+                        s2 = so;
+                        i2 = io;
+                        rk = ro;
+                    }
+                }
+                if (lane == 0) {
+                    sh.piv = (s2 > 0.0) ? i2 : j;  // all-zero column: no interchange
+                    sh.winner = (s2 > 0.0) ? rk : owner_rank(j);
+                }
+            }
+            __syncthreads();
+            const int piv = sh.piv;
+            if (tid < W) {
+                RegPanelShared<W>* ds = cluster.map_shared_rank(&sh, owner_rank(j));
+                const double ojr = ds->diag_vals[par][0][tid], oji = ds->diag_vals[par][1][tid];
+                if (piv == j) {
+                    sh.ur[tid] = ojr;
+                    sh.ui[tid] = oji;
+                } else {
+                    RegPanelShared<W>* ws = cluster.map_shared_rank(&sh, sh.winner);
+                    sh.ur[tid] = ws->cand_vals[par][0][tid];
+                    sh.ui[tid] = ws->cand_vals[par][1][tid];
+                }
+                sh.ojr[tid] = ojr;
+                sh.oji[tid] = oji;
+            }
+            if (rank == 0 && tid == 0) {
+                sh.pivs[q * W + jj] = piv;
+                ipiv[(long)b * N + j] = piv;
+            }
+            __syncthreads();
+            const cplx pv{sh.ur[jj], sh.ui[jj]};
+            const bool nonzero = (pv.re != 0.0 || pv.im != 0.0);
+            const cplx inv = nonzero ? crecip(pv) : cplx{0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i) {
+                if (!has[i]) continue;
+                if (row[i] == j) {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        xr[i][k] = sh.ur[k];
+                        xi[i][k] = sh.ui[k];
+                    }
+                } else if (row[i] > j) {
+                    if (row[i] == piv) {
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            xr[i][k] = sh.ojr[k];
+                            xi[i][k] = sh.oji[k];
+                        }
+                    }
+                    cplx l{xr[i][jj], xi[i][jj]};
+                    if (nonzero) {
+                        l = cmul(l, inv);
+                        xr[i][jj] = l.re;
+                        xi[i][jj] = l.im;
+                    }
+#pragma unroll
+                    for (int k = jj + 1; k < W; ++k) {
+                        const double ur = sh.ur[k], ui = sh.ui[k];
+                        xr[i][k] -= l.re * ur - l.im * ui;
+                        xi[i][k] -= l.re * ui + l.im * ur;
+                    }
+                }
+            }
+        }
+        // ---- store the factored leaf
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i)
+            if (has[i] && row[i] >= c0)
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    Fr[at(row[i], c0 + k)] = xr[i][k];
+                    Fi[at(row[i], c0 + k)] = xi[i][k];
+                }
+        cluster.sync();
+        // ---- rank 0: apply the leaf's interchanges to the other panel columns
+        if (rank == 0) {
+            __shared__ int s_cnt;
+            if (wid == 0) {
+                const int cnt = net_permutation(sh, c0, sh.pivs + q * W, W, lane);
+                if (lane == 0) s_cnt = cnt;
+            }
+            __syncthreads();
+            const int cnt = s_cnt;
+            const int other = PWID - W;
+            for (int e = tid; e < cnt * other; e += NT) {
+                const int m = e % cnt, c = e / cnt;
+                const int col = k0 + (c < q * W ? c : c + W);
+                sh.gr[m][c] = Fr[at(sh.tsrc[m], col)];
+                sh.gi[m][c] = Fi[at(sh.tsrc[m], col)];
+            }
+            __syncthreads();
+            for (int e = tid; e < cnt * other; e += NT) {
+                const int m = e % cnt, c = e / cnt;
+                const int col = k0 + (c < q * W ? c : c + W);
+                Fr[at(sh.tpos[m], col)] = sh.gr[m][c];
+                Fi[at(sh.tpos[m], col)] = sh.gi[m][c];
+            }
+        }
+        cluster.sync();
+        if (q == PWID / W - 1) break;
+        // ---- leaf U block: U = Lqq^{-1} T, T = rows [c0, c0+W) x cols [c0+W, k0+64)
+        const int rc0 = c0 + W;
+        const int nrc = k0 + PWID - rc0;
+        for (int e = tid; e < W * W; e += NT) {
+            const int i = e % W, k = e / W;
+            sh.lr[i][k] = Fr[at(c0 + i, c0 + k)];
+            sh.li[i][k] = Fi[at(c0 + i, c0 + k)];
+        }
+        for (int e = tid; e < W * nrc; e += NT) {
+            const int i = e % W, c = e / W;
+            sh.Ur[i][c] = Fr[at(c0 + i, rc0 + c)];
+            sh.Ui[i][c] = Fi[at(c0 + i, rc0 + c)];
+        }
+        __syncthreads();
+        for (int r = 0; r < W - 1; ++r) {  // forward substitution, unit lower
+            for (int e = tid; e < (W - 1 - r) * nrc; e += NT) {
+                const int i = r + 1 + e % (W - 1 - r), c = e / (W - 1 - r);
+                const double lr = sh.lr[i][r], li = sh.li[i][r];
+                const double xr0 = sh.Ur[r][c], xi0 = sh.Ui[r][c];
+                sh.Ur[i][c] -= lr * xr0 - li * xi0;
+                sh.Ui[i][c] -= lr * xi0 + li * xr0;
+            }
+            __syncthreads();
+        }
+        if (rank == 0)
+            for (int e = tid; e < W * nrc; e += NT) {
+                const int i = e % W, c = e / W;
+                Fr[at(c0 + i, rc0 + c)] = sh.Ur[i][c];
+                Fi[at(c0 + i, rc0 + c)] = sh.Ui[i][c];
+            }
+        // ---- own rows >= rc0: A[row, rc0:] -= L[row, leaf] U
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+            if (!has[i] || row[i] < rc0) continue;
+            for (int cb = 0; cb < nrc; cb += 8) {
+                double ar[8], ai[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (cb + t < nrc) {
+                        ar[t] = Fr[at(row[i], rc0 + cb + t)];
+                        ai[t] = Fi[at(row[i], rc0 + cb + t)];
+                    }
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const double lr = xr[i][k], li = xi[i][k];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if (cb + t < nrc) {
+                            const double ur = sh.Ur[k][cb + t], ui = sh.Ui[k][cb + t];
+                            ar[t] -= lr * ur - li * ui;
+                            ai[t] -= lr * ui + li * ur;
+                        }
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (cb + t < nrc) {
+                        Fr[at(row[i], rc0 + cb + t)] = ar[t];
+                        Fi[at(row[i], rc0 + cb + t)] = ai[t];
+                    }
+            }
+        }
+        __syncthreads();
+    }
+    // ---- rank 0: net permutation of all 64 interchanges for the outer laswp
+    if (rank == 0 && wid == 0) {
+        const int cnt = net_permutation(sh, k0, sh.pivs, PWID, lane);
+        int* tab = ptab + (long)b * (4 * PWID + 1);
+        if (lane == 0) tab[0] = cnt;
+        for (int m = lane; m < cnt; m += 32) {
+            tab[1 + m] = sh.tpos[m];
+            tab[1 + 2 * PWID + m] = sh.tsrc[m];
+        }
+    }
+    cluster.sync();  // shared memory stays alive until every CTA is done with it
+}
+
+template <int W, int ROWS, int NT>
+static void launch_reg(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+    const size_t sm = sizeof(RegPanelShared<W>);
+    ensure_smem((const void*)panel_reg_kernel<W, ROWS, NT>, sm);
+    panel_reg_kernel<W, ROWS, NT><<<dim3(PCL2, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab);
+}
+
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+    const int R = (N - k0 + PCL2 - 1) / PCL2;
+    if (R <= 256)
+        launch_reg<16, 1, 256>(F, N, k0, ipiv, ptab, batch, s);
+    else if (R <= 512)
+        launch_reg<16, 1, 512>(F, N, k0, ipiv, ptab, batch, s);
+    else if (R <= 1024)
+        launch_reg<8, 2, 512>(F, N, k0, ipiv, ptab, batch, s);
+    else if (R <= 2048)
+        launch_reg<4, 4, 512>(F, N, k0, ipiv, ptab, batch, s);
+    else
+        launch_reg<2, 8, 512>(F, N, k0, ipiv, ptab, batch, s);
+}
+
+}  // namespace fl
