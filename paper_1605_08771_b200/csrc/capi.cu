@@ -534,6 +534,41 @@ void ensure_rr_scratch(fl_ctx* ctx) {
     ctx->scal.ensure(64);
 }
 
+// ColPivHouseholderQR(X) with threshold thr (proj/src/ritz.cpp:22-29,
+// drivers.cpp:33-36): rank = #{|R_kk| > thr * max |R_jj|}; if U is given it
+// receives the first `rank` columns of Q.
+int colpiv_qr(fl_ctx* ctx, const fl_block* X, double thr, fl_block* U) {
+    const int n = X->n, N = X->N, p = X->cols;
+    const int kmax = std::min(n, p);
+    double* Aw = scratch(ctx->rr_nxp, (size_t)N * std::max(p, 1));
+    double* tau = scratch(ctx->vals_d, std::max(kmax, 1));
+    double* vn = scratch(ctx->norms_d, 2 * (size_t)std::max(p, 1));
+    int* jpvt = reinterpret_cast<int*>(scratch(ctx->idx_d, std::max(p, 1)));
+    CK(cudaMemcpyAsync(Aw, X->d(), sizeof(double) * (size_t)N * p, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    if (launch_qr(Aw, N, n, p, tau, jpvt, vn, vn + p, ctx->stream) != 0)
+        throw Fail{FL_CUDA, "colpiv_qr: cooperative launch failed"};
+    g_launch_count += 1;
+    std::vector<double> diag(kmax);
+    CK(cudaMemcpy2DAsync(diag.data(), sizeof(double), Aw, sizeof(double) * (N + 1), sizeof(double),
+                         kmax, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    double maxpivot = 0.0;
+    for (double d : diag) maxpivot = std::max(maxpivot, std::abs(d));
+    int r = 0;
+    for (double d : diag)
+        if (std::abs(d) > maxpivot * thr) ++r;
+    if (U && r > 0) {
+        block_reserve(U, r);
+        block_set_cols(U, r);
+        if (launch_orgqr(Aw, N, tau, n, r, U->d(), U->ld(), ctx->stream) != 0)
+            throw Fail{FL_CUDA, "colpiv_qr: cooperative launch failed"};
+        g_launch_count += 1;
+        sync(ctx);
+    }
+    return r;
+}
+
 void orthonormalize_dev(fl_ctx* ctx, const fl_block* X, double drop_tol, fl_block* U, int* rank_out) {
     const int p = X->cols, N = X->N, n = X->n;
     if (p < 1 || n < 1) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: empty block"};
@@ -796,6 +831,11 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
 
+int fl_debug_panel_profile(double* out8, int reset) {
+    panel_profile(out8, reset != 0);
+    return FL_OK;
+}
+
 int fl_ctx_set_streams(fl_ctx* ctx, int n) {
     CtxLock lk(ctx);
     ctx->nstreams = std::max(1, std::min(n, (int)ctx->aux.size()));
@@ -1028,12 +1068,15 @@ int fl_orthonormalize(fl_ctx* ctx, const fl_block* X, double drop_tol, int metho
                       int* rank, fl_err* err) {
     return guarded(err, [&] {
         if (X->cols < 1 || X->n < 1) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: empty block"};
-        if (method != 0)
-            throw Fail{FL_INVALID_ARGUMENT,
-                       "orthonormalize: the qr orthogonalizer is not implemented on the device yet"};
         if (X == U) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: X and U must differ"};
         CtxLock lk(ctx);
-        orthonormalize_dev(ctx, X, drop_tol, U, rank);
+        if (method == 1) {
+            const int r = colpiv_qr(ctx, X, drop_tol, U);
+            if (r == 0) throw Fail{FL_RUNTIME_ERROR, "orthonormalize: block is numerically zero"};
+            *rank = r;
+        } else {
+            orthonormalize_dev(ctx, X, drop_tol, U, rank);
+        }
     });
 }
 
@@ -1075,32 +1118,11 @@ int fl_residual_block(fl_ctx* ctx, const fl_matrix* A, const fl_block* V, const 
 int fl_block_rank(fl_ctx* ctx, const fl_block* X, double threshold, int* rank, fl_err* err) {
     return guarded(err, [&] {
         CtxLock lk(ctx);
-        const int p = X->cols, N = X->N;
-        if (p < 1) {
+        if (X->cols < 1) {
             *rank = 0;
             return;
         }
-        const int P = round_up(p, FL_TILE);
-        ensure_rr_scratch(ctx);
-        double* G = scratch(ctx->s1, (size_t)P * P);
-        double* Gs = scratch(ctx->s2, (size_t)P * P);
-        double* work = scratch(ctx->s3, (size_t)P * P);
-        double* V = scratch(ctx->s4, (size_t)P * P);
-        double* Vt = scratch(ctx->s5, (size_t)P * P);
-        double* vals = scratch(ctx->vals_d, P);
-        launch_dgemm(DGemm{P, P, N, X->d(), X->ld(), 0, X->d(), X->ld(), 0, G, P, 0, 1.0, 0.0}, true,
-                     false, 1, ctx->stream);
-        launch_symmetrize(G, P, p, Gs, P, ctx->stream);
-        device_sym_eig(ctx, Gs, P, p, P, vals, V, work, Vt);
-        std::vector<double> ev(p);
-        CK(cudaMemcpyAsync(ev.data(), vals, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
-        // singular values sigma_i = sqrt(ev_i); rank = #{sigma_i > threshold * sigma_max}
-        const double smax = std::sqrt(std::max(0.0, ev[p - 1]));
-        int r = 0;
-        for (int i = 0; i < p; ++i)
-            if (std::sqrt(std::max(0.0, ev[i])) > threshold * smax) ++r;
-        *rank = r;
+        *rank = colpiv_qr(ctx, X, threshold, nullptr);
     });
 }
 

@@ -51,6 +51,8 @@ void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& 
 // Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j];
 // ptab[b*257 ...] receives the panel's net row permutation (count, rows, sources).
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s);
+// Cycle counts of the panel kernel phases (node 0, rank 0, thread 0).
+void panel_profile(double* out8, bool reset);
 // Apply the panel's 64 row interchanges (ptab) to all columns outside the panel.
 void launch_laswp_panel(ZBatch F, int N, int k0, const int* ptab, int batch, cudaStream_t s);
 // Inverses of `nblocks` consecutive 64x64 diagonal blocks starting at (r0, r0):

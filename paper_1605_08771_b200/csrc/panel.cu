@@ -95,6 +95,18 @@ __device__ int net_permutation(SH& sh, int first, const int* piv, int count, int
 
 }  // namespace
 
+__device__ unsigned long long g_panel_prof[8];
+
+void panel_profile(double* out8, bool reset) {
+    unsigned long long h[8];
+    cudaMemcpyFromSymbol(h, g_panel_prof, sizeof(h));
+    for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_panel_prof, z, sizeof(z));
+    }
+}
+
 template <int W, int ROWS, int NT>
 __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
     panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
@@ -122,6 +134,15 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
         has[i] = row[i] < top;
     }
     double xr[ROWS][W], xi[ROWS][W];
+    // phase timing of node 0 / rank 0 / thread 0 (fl_debug_panel_profile)
+    const bool prof_on = (b == 0 && rank == 0 && tid == 0);
+    long long t_last = clock64();
+#define PPROF(k)                                                                 \
+    if (prof_on) {                                                               \
+        const long long t_ = clock64();                                          \
+        atomicAdd(&g_panel_prof[k], (unsigned long long)(t_ - t_last));          \
+        t_last = t_;                                                             \
+    }
 
     for (int q = 0; q < PWID / W; ++q) {
         const int c0 = k0 + q * W;
@@ -138,7 +159,9 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                     xi[i][k] = 0.0;
                 }
         // ---- column steps
-#pragma unroll
+        // not unrolled (instruction-cache footprint): register entries are
+        // addressed with compile-time k and runtime predicates on jj
+#pragma unroll 1
         for (int jj = 0; jj < W; ++jj) {
             const int j = c0 + jj;
             const int par = j & 1;
@@ -148,7 +171,14 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
 #pragma unroll
             for (int i = 0; i < ROWS; ++i)
                 if (has[i] && row[i] >= j) {
-                    const double sc = xr[i][jj] * xr[i][jj] + xi[i][jj] * xi[i][jj];
+                    double pr = 0.0, pi = 0.0;
+#pragma unroll
+                    for (int k = 0; k < W; ++k)
+                        if (k == jj) {
+                            pr = xr[i][k];
+                            pi = xi[i][k];
+                        }
+                    const double sc = pr * pr + pi * pi;
                     if (better(sc, row[i], s, idx)) {
                         s = sc;
                         idx = row[i];
@@ -188,7 +218,9 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                         }
                 }
             }
+            PPROF(0);
             cluster.sync();
+            PPROF(1);
             if (wid == 0) {
                 double s2 = -1.0;
                 int i2 = 0x7fffffff, rk = lane;
@@ -238,6 +270,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                 ipiv[(long)b * N + j] = piv;
             }
             __syncthreads();
+            PPROF(2);
             const cplx pv{sh.ur[jj], sh.ui[jj]};
             const bool nonzero = (pv.re != 0.0 || pv.im != 0.0);
             const cplx inv = nonzero ? crecip(pv) : cplx{0.0, 0.0};
@@ -258,20 +291,25 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                             xi[i][k] = sh.oji[k];
                         }
                     }
-                    cplx l{xr[i][jj], xi[i][jj]};
-                    if (nonzero) {
-                        l = cmul(l, inv);
-                        xr[i][jj] = l.re;
-                        xi[i][jj] = l.im;
-                    }
+                    cplx l{0.0, 0.0};
 #pragma unroll
-                    for (int k = jj + 1; k < W; ++k) {
-                        const double ur = sh.ur[k], ui = sh.ui[k];
-                        xr[i][k] -= l.re * ur - l.im * ui;
-                        xi[i][k] -= l.re * ui + l.im * ur;
+                    for (int k = 0; k < W; ++k)
+                        if (k == jj) l = cplx{xr[i][k], xi[i][k]};
+                    if (nonzero) l = cmul(l, inv);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        if (k == jj) {
+                            xr[i][k] = l.re;
+                            xi[i][k] = l.im;
+                        } else if (k > jj) {
+                            const double ur = sh.ur[k], ui = sh.ui[k];
+                            xr[i][k] -= l.re * ur - l.im * ui;
+                            xi[i][k] -= l.re * ui + l.im * ur;
+                        }
                     }
                 }
             }
+            PPROF(3);
         }
         // ---- store the factored leaf
 #pragma unroll
@@ -283,6 +321,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                     Fi[at(row[i], c0 + k)] = xi[i][k];
                 }
         cluster.sync();
+        PPROF(4);
         // ---- rank 0: apply the leaf's interchanges to the other panel columns
         if (rank == 0) {
             __shared__ int s_cnt;
@@ -308,6 +347,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
             }
         }
         cluster.sync();
+        PPROF(5);
         if (q == PWID / W - 1) break;
         // ---- leaf U block: U = Lqq^{-1} T, T = rows [c0, c0+W) x cols [c0+W, k0+64)
         const int rc0 = c0 + W;
@@ -339,6 +379,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                 Fr[at(c0 + i, rc0 + c)] = sh.Ur[i][c];
                 Fi[at(c0 + i, rc0 + c)] = sh.Ui[i][c];
             }
+        PPROF(6);
         // ---- own rows >= rc0: A[row, rc0:] -= L[row, leaf] U
 #pragma unroll
         for (int i = 0; i < ROWS; ++i) {
@@ -371,6 +412,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
             }
         }
         __syncthreads();
+        PPROF(7);
     }
     // ---- rank 0: net permutation of all 64 interchanges for the outer laswp
     if (rank == 0 && wid == 0) {

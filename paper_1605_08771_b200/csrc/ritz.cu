@@ -530,3 +530,211 @@ int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, 
 }
 
 }  // namespace fl
+
+namespace fl {
+
+// ------------------------------------------------------------------ column-pivoted Householder QR
+// ColPivHouseholderQR stand-in (proj/src/ritz.cpp:22-29, drivers.cpp:33-36),
+// LAPACK dgeqp3/dlaqp2 semantics: pivot = largest remaining partial column
+// norm (first on ties), Householder beta = -sign(alpha) ||x||, partial norms
+// downdated with the sqrt(eps) recompute guard. One cooperative kernel: per
+// step, CTA 0 picks the pivot, swaps and forms the reflector; every CTA then
+// applies it to its share of the trailing columns (2 grid barriers / step).
+struct QRArgs {
+    double* A;
+    long lda;
+    int n, p, kmax;
+    double* tau;   // [kmax]
+    int* jpvt;     // [p]
+    double* vn1;   // [p] partial norms
+    double* vn2;   // [p] reference norms
+};
+
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    return t;
+}
+
+__global__ void __launch_bounds__(256) qr_kernel(QRArgs q) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[32];
+    __shared__ int s_piv;
+    __shared__ double s_beta, s_scale;
+    const long lda = q.lda;
+    // initial norms
+    for (int j = blockIdx.x; j < q.p; j += gridDim.x) {
+        double s = 0.0;
+        for (int i = threadIdx.x; i < q.n; i += blockDim.x) s += q.A[(long)j * lda + i] * q.A[(long)j * lda + i];
+        s = block_sum(s, red);
+        if (threadIdx.x == 0) {
+            q.vn1[j] = sqrt(s);
+            q.vn2[j] = sqrt(s);
+            q.jpvt[j] = j;
+        }
+    }
+    grid.sync();
+    const double tol3z = sqrt(2.220446049250313e-16);
+    for (int k = 0; k < q.kmax; ++k) {
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) {
+                int pv = k;
+                double best = q.vn1[k];
+                for (int j = k + 1; j < q.p; ++j)
+                    if (q.vn1[j] > best) { best = q.vn1[j]; pv = j; }
+                s_piv = pv;
+                if (pv != k) {
+                    const int t = q.jpvt[k];
+                    q.jpvt[k] = q.jpvt[pv];
+                    q.jpvt[pv] = t;
+                    q.vn1[pv] = q.vn1[k];
+                    q.vn2[pv] = q.vn2[k];
+                }
+            }
+            __syncthreads();
+            const int pv = s_piv;
+            double* ck = q.A + (long)k * lda;
+            if (pv != k) {
+                double* cp = q.A + (long)pv * lda;
+                for (int i = threadIdx.x; i < q.n; i += blockDim.x) {
+                    const double t = ck[i];
+                    ck[i] = cp[i];
+                    cp[i] = t;
+                }
+            }
+            __syncthreads();
+            // reflector for column k (dlarfg)
+            double s = 0.0;
+            for (int i = k + 1 + threadIdx.x; i < q.n; i += blockDim.x) s += ck[i] * ck[i];
+            const double xnorm = sqrt(block_sum(s, red));
+            if (threadIdx.x == 0) {
+                const double alpha = ck[k];
+                if (xnorm == 0.0) {
+                    q.tau[k] = 0.0;
+                    s_beta = alpha;
+                    s_scale = 1.0;
+                } else {
+                    const double beta = -copysign(hypot(alpha, xnorm), alpha);
+                    q.tau[k] = (beta - alpha) / beta;
+                    s_beta = beta;
+                    s_scale = 1.0 / (alpha - beta);
+                }
+            }
+            __syncthreads();
+            if (q.tau[k] != 0.0)
+                for (int i = k + 1 + threadIdx.x; i < q.n; i += blockDim.x) ck[i] *= s_scale;
+            __syncthreads();
+            if (threadIdx.x == 0) ck[k] = s_beta;
+        }
+        grid.sync();
+        // apply H_k = I - tau v v^T (v_k = 1) to columns k+1.. and downdate norms
+        const double tk = q.tau[k];
+        const double* v = q.A + (long)k * lda;
+        for (int j = k + 1 + blockIdx.x; j < q.p; j += gridDim.x) {
+            double* cj = q.A + (long)j * lda;
+            if (tk != 0.0) {
+                double s = (threadIdx.x == 0) ? cj[k] : 0.0;
+                for (int i = k + 1 + threadIdx.x; i < q.n; i += blockDim.x) s += v[i] * cj[i];
+                const double w = tk * block_sum(s, red);
+                if (threadIdx.x == 0) cj[k] -= w;
+                for (int i = k + 1 + threadIdx.x; i < q.n; i += blockDim.x) cj[i] -= w * v[i];
+                __syncthreads();
+            }
+            const double v1 = q.vn1[j], v2 = q.vn2[j], rkj = cj[k];
+            __syncthreads();
+            if (v1 != 0.0) {  // dlaqp2 norm downdate
+                double temp = fabs(rkj) / v1;
+                temp = fmax(0.0, 1.0 - temp * temp);
+                const double r = v1 / v2;
+                const double temp2 = temp * r * r;
+                if (temp2 <= tol3z) {
+                    double s = 0.0;
+                    for (int i = k + 1 + threadIdx.x; i < q.n; i += blockDim.x) s += cj[i] * cj[i];
+                    const double nr = sqrt(block_sum(s, red));
+                    if (threadIdx.x == 0) {
+                        q.vn1[j] = nr;
+                        q.vn2[j] = nr;
+                    }
+                } else if (threadIdx.x == 0) {
+                    q.vn1[j] = v1 * sqrt(temp);
+                }
+            }
+            __syncthreads();
+        }
+        grid.sync();
+    }
+}
+
+// Q[:, 0:r] = H_0 ... H_{r-1} I[:, 0:r] (dorg2r), reflectors in A below the diagonal
+struct OrgArgs {
+    const double* A;
+    long lda;
+    const double* tau;
+    double* Q;
+    long ldq;
+    int n, r;
+};
+
+__global__ void __launch_bounds__(256) orgqr_kernel(OrgArgs o) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[32];
+    for (int j = blockIdx.x; j < o.r; j += gridDim.x)
+        for (int i = threadIdx.x; i < o.n; i += blockDim.x)
+            o.Q[(long)j * o.ldq + i] = (i == j) ? 1.0 : 0.0;
+    grid.sync();
+    for (int k = o.r - 1; k >= 0; --k) {
+        const double tk = o.tau[k];
+        const double* v = o.A + (long)k * o.lda;
+        if (tk != 0.0)
+            for (int j = k + blockIdx.x; j < o.r; j += gridDim.x) {
+                double* qj = o.Q + (long)j * o.ldq;
+                double s = (threadIdx.x == 0) ? qj[k] : 0.0;
+                for (int i = k + 1 + threadIdx.x; i < o.n; i += blockDim.x) s += v[i] * qj[i];
+                const double w = tk * block_sum(s, red);
+                if (threadIdx.x == 0) qj[k] -= w;
+                for (int i = k + 1 + threadIdx.x; i < o.n; i += blockDim.x) qj[i] -= w * v[i];
+                __syncthreads();
+            }
+        grid.sync();
+    }
+}
+
+static int coop_blocks(const void* fn, int work) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+    int blocks = nsm * (per_sm > 0 ? 1 : 1);
+    if (work < blocks) blocks = work > 0 ? work : 1;
+    return blocks;
+}
+
+int launch_qr(double* A, long lda, int n, int p, double* tau, int* jpvt, double* vn1, double* vn2,
+              cudaStream_t s) {
+    QRArgs q{A, lda, n, p, n < p ? n : p, tau, jpvt, vn1, vn2};
+    void* args[] = {&q};
+    const int blocks = coop_blocks((const void*)qr_kernel, p);
+    return cudaLaunchCooperativeKernel((const void*)qr_kernel, dim3(blocks), dim3(256), args, 0, s) ==
+                   cudaSuccess
+               ? 0
+               : -1;
+}
+
+int launch_orgqr(const double* A, long lda, const double* tau, int n, int r, double* Q, long ldq,
+                 cudaStream_t s) {
+    if (r <= 0) return 0;
+    OrgArgs o{A, lda, tau, Q, ldq, n, r};
+    void* args[] = {&o};
+    const int blocks = coop_blocks((const void*)orgqr_kernel, r);
+    return cudaLaunchCooperativeKernel((const void*)orgqr_kernel, dim3(blocks), dim3(256), args, 0,
+                                       s) == cudaSuccess
+               ? 0
+               : -1;
+}
+
+}  // namespace fl

@@ -27,4 +27,12 @@ int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, 
                double* vals, double* Vout, long ldo, int* scratch_int, unsigned long long* counters,
                int max_sweeps, cudaStream_t s);
 
+// In-place column-pivoted Householder QR (dgeqp3 semantics) of the n x p matrix
+// A; tau[min(n,p)], jpvt[p], norm scratch vn1/vn2[p]. Returns 0 on success.
+int launch_qr(double* A, long lda, int n, int p, double* tau, int* jpvt, double* vn1, double* vn2,
+              cudaStream_t s);
+// Q[:, 0:r] of the reflectors left in A by launch_qr.
+int launch_orgqr(const double* A, long lda, const double* tau, int n, int r, double* Q, long ldq,
+                 cudaStream_t s);
+
 }  // namespace fl

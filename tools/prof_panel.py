@@ -1,0 +1,33 @@
+import sys, time
+import numpy as np
+sys.path.insert(0, '.')
+import paper_1605_08771_b200 as P
+ctx = P.default_context()
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+A = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n)))
+A = 0.5 * (A + A.T) / np.sqrt(n)
+X = np.asfortranarray(np.random.default_rng(1).standard_normal((n, 64)))
+for nc in (1, 4, 16):
+    rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.2), nc)
+    f = P.FilterApplier(A, rule, ctx=ctx)
+    f.apply(X)
+    for streams in (1, 4):
+        ctx.set_streams(streams)
+        ctx.set_profiling(True)
+        t0 = time.time(); f.apply(X); t1 = time.time()
+        out = {k: ctx.profile(k) for k in ("panel", "laswp", "trsm", "zgemm")}
+        ctx.set_profiling(False)
+        print(f"n={n} nc={nc} streams={streams} wall={1e3*(t1-t0):.1f}ms " +
+              " ".join(f"{k}:{v[0]:.1f}ms/{v[2]}" for k, v in out.items()), flush=True)
+import ctypes
+from paper_1605_08771_b200 import _lib
+out = (ctypes.c_double * 8)()
+_lib.lib().fl_debug_panel_profile(out, 1)
+rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.2), 1)
+f = P.FilterApplier(A, rule, ctx=ctx)
+f.apply(X)
+_lib.lib().fl_debug_panel_profile(out, 1)
+names = ["cand+publish", "cluster.sync", "pivot fetch", "update", "leaf store+sync", "perm+sync", "trsm", "inner update"]
+tot = sum(out)
+print("panel phases (cycles, 1 node, all panels):", {k: int(v) for k, v in zip(names, out)}, "total", int(tot),
+      "-> us per column", tot / 1.965e3 / n)
