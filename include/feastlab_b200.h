@@ -83,6 +83,9 @@ long long fl_ctx_launches(const fl_ctx* ctx);
 int fl_ctx_set_profiling(fl_ctx* ctx, int on);
 /* number of contour-node chunks factored/solved concurrently (1..4, default 4) */
 int fl_ctx_set_streams(fl_ctx* ctx, int n);
+/* timeline of the profiled launches: out[3i] = class index (order of
+   fl_ctx_profile's classes), out[3i+1] / out[3i+2] = start / end in ms */
+int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records);
 /* cycle counts of the LU panel kernel's phases (instrumentation) */
 int fl_debug_panel_profile(double* out8, int reset);
 int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,

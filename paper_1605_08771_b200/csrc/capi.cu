@@ -89,9 +89,10 @@ struct DBuf {
 // Per-kernel-class CUDA-event timing (fl_ctx_set_profiling): bench.py's
 // roofline numbers come from these events, recorded on the launch stream.
 enum ProfClass { P_SHIFT, P_PANEL, P_LASWP, P_TRSM, P_ZGEMM, P_PERMUTE, P_ACCUM, P_ALLREDUCE,
-                 P_NCLASS };
+                 P_EIG, P_ORTH, P_RR, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"shift",   "panel",      "laswp",    "trsm",
-                                          "zgemm",   "permute",    "accumulate", "allreduce"};
+                                          "zgemm",   "permute",    "accumulate", "allreduce",
+                                          "eig",     "orthonormalize", "rayleigh_ritz"};
 
 struct Profiler {
     struct Rec {
@@ -133,6 +134,8 @@ struct fl_ctx {
     std::vector<cudaStream_t> aux;  // node-chunk streams (fork/join on `stream`)
     cudaEvent_t fork = nullptr;
     std::vector<cudaEvent_t> join;
+    std::vector<cudaStream_t> paux;  // per chunk: look-ahead panel stream (high priority)
+    std::vector<cudaEvent_t> ev_panel, ev_next;
     int nstreams = 4;  // node chunks in flight (<= aux.size())
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
@@ -254,7 +257,13 @@ struct Prof {
 
 // --------------------------------------------------------------- filter core
 // Factor nodes [g0, g0+G) of the local range into factor slots [s0, s0+G).
-void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
+// Look-ahead: stream `st` runs the swaps and the trailing update; stream `sp`
+// factors panel k+1 as soon as its 64 columns are updated (GEMM "next"),
+// concurrently with the rest of update k (GEMM "rest").
+//   st: wait(P_k) laswp_k  U12_k  GEMM_next_k  rec(N_k)  GEMM_rest_k
+//   sp: wait(N_{k-1})  panel_k  trinv(L_kk)  rec(P_k)
+void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStream_t sp,
+                  cudaEvent_t ev_panel, cudaEvent_t ev_next) {
     fl_ctx* ctx = f->ctx;
     const int N = f->A->N, n = f->A->n;
     const long stride = (long)N * N;
@@ -273,12 +282,16 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
         Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
         launch_shift(f->A->d(), N, N, F, z, G, st);
     }
+    CK(cudaEventRecord(ev_next, st));  // shift done: panel 0 may start
     for (int k0 = 0; k0 < N; k0 += FL_TILE) {
         {
-            Prof pr(ctx, P_PANEL, 0.0, 2, st);
-            launch_panel(F, N, k0, ipiv, ptab, G, st);
-            launch_trinv(F, k0, 1, false, Inv, k0 / FL_TILE, G, st);
+            CK(cudaStreamWaitEvent(sp, ev_next, 0));
+            Prof pr(ctx, P_PANEL, 0.0, 2, sp);
+            launch_panel(F, N, k0, ipiv, ptab, G, sp);
+            launch_trinv(F, k0, 1, false, Inv, k0 / FL_TILE, G, sp);
         }
+        CK(cudaEventRecord(ev_panel, sp));
+        CK(cudaStreamWaitEvent(st, ev_panel, 0));
         {
             Prof pr(ctx, P_LASWP, 0.0, 1, st);
             launch_laswp_panel(F, N, k0, ptab, G, st);
@@ -297,13 +310,20 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st) {
                         N, stride};
                 launch_zgemm_set(u, G, st);
             }
-            ZGemm g{rest, rest, FL_TILE,
-                    F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N, stride,
-                    F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0, N, stride,
-                    F.re + (long)(k0 + FL_TILE) * N + k0 + FL_TILE,
-                    F.im + (long)(k0 + FL_TILE) * N + k0 + FL_TILE, N, stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * rest * rest * FL_TILE * G, 1, st);
-            launch_zgemm_sub(g, G, st);
+            // trailing update A22 -= L21 U12, split: next panel's columns first
+            auto upd = [&](int c0, int nc) {
+                ZGemm g{rest, nc, FL_TILE,
+                        F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N,
+                        stride,
+                        F.re + (long)c0 * N + k0, F.im + (long)c0 * N + k0, N, stride,
+                        F.re + (long)c0 * N + k0 + FL_TILE, F.im + (long)c0 * N + k0 + FL_TILE, N,
+                        stride};
+                Prof pr(ctx, P_ZGEMM, 8.0 * rest * nc * FL_TILE * G, 1, st);
+                launch_zgemm_sub(g, G, st);
+            };
+            upd(k0 + FL_TILE, FL_TILE);
+            CK(cudaEventRecord(ev_next, st));
+            if (rest > FL_TILE) upd(k0 + 2 * FL_TILE, rest - FL_TILE);
         }
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
@@ -424,7 +444,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
                 if (f->factored[g]) { ++g; continue; }
                 int e = g;
                 while (e < c1 && !f->factored[e]) ++e;
-                factor_group(f, g, e - g, g, ctx->aux[j]);
+                factor_group(f, g, e - g, g, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
+                             ctx->ev_next[j]);
                 for (int k = g; k < e; ++k) f->factored[k] = 1;
                 new_facts += e - g;
                 g = e;
@@ -439,7 +460,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             for (int j = 0; j < nsr; ++j) {
                 const int c0 = (int)((long)G * j / nsr), c1 = (int)((long)G * (j + 1) / nsr);
                 const int s0 = (int)((long)slots * j / ns);
-                factor_group(f, g + c0, c1 - c0, s0, ctx->aux[j]);
+                factor_group(f, g + c0, c1 - c0, s0, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
+                             ctx->ev_next[j]);
                 solve_group(f, g + c0, c1 - c0, s0, X, ldx, P, ctx->aux[j]);
             }
         }
@@ -513,6 +535,7 @@ double* scratch(DBuf& b, size_t doubles) {
 // ascending vals (device), vectors into V (P x P zero-padded, ld P).
 void device_sym_eig(fl_ctx* ctx, double* M, long ldm, int p, int P, double* vals, double* V,
                     double* work, double* Vtmp) {
+    Prof pr(ctx, P_EIG, (double)p, 0);
     launch_fro2(M, ldm, p, ctx->scal.d(), ctx->stream);
     double fro2 = 0.0;
     CK(cudaMemcpyAsync(&fro2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -570,6 +593,7 @@ int colpiv_qr(fl_ctx* ctx, const fl_block* X, double thr, fl_block* U) {
 }
 
 void orthonormalize_dev(fl_ctx* ctx, const fl_block* X, double drop_tol, fl_block* U, int* rank_out) {
+    Prof pr(ctx, P_ORTH, (double)X->cols, 0);
     const int p = X->cols, N = X->N, n = X->n;
     if (p < 1 || n < 1) throw Fail{FL_INVALID_ARGUMENT, "orthonormalize: empty block"};
     const int P = round_up(p, FL_TILE);
@@ -637,6 +661,7 @@ struct RRResult {
 
 void rayleigh_ritz_dev(fl_ctx* ctx, const fl_matrix* A, const fl_block* X, double lo, double hi,
                        fl_block* Vout, RRResult& out) {
+    Prof pr(ctx, P_RR, (double)X->cols, 0);
     const int p = X->cols, N = X->N, n = X->n;
     if (n != A->n) throw Fail{FL_INVALID_ARGUMENT, "rayleigh_ritz: block/matrix dimension mismatch"};
     if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "rayleigh_ritz: empty block"};
@@ -760,11 +785,20 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         const int naux = 4;
+        int prio_lo = 0, prio_hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         c->aux.resize(naux);
+        c->paux.resize(naux);
         c->join.resize(naux);
+        c->ev_panel.resize(naux);
+        c->ev_next.resize(naux);
         for (int j = 0; j < naux; ++j) {
             CK(cudaStreamCreateWithFlags(&c->aux[j], cudaStreamNonBlocking));
+            // panels are the critical path: highest priority
+            CK(cudaStreamCreateWithPriority(&c->paux[j], cudaStreamNonBlocking, prio_hi));
             CK(cudaEventCreateWithFlags(&c->join[j], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_panel[j], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_next[j], cudaEventDisableTiming));
         }
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         c->rank = rank;
@@ -808,6 +842,12 @@ int fl_ctx_destroy(fl_ctx* ctx) {
         cudaStreamDestroy(a);
     }
     for (cudaEvent_t e : ctx->join) cudaEventDestroy(e);
+    for (cudaStream_t a : ctx->paux) {
+        cudaStreamSynchronize(a);
+        cudaStreamDestroy(a);
+    }
+    for (cudaEvent_t e : ctx->ev_panel) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->ev_next) cudaEventDestroy(e);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -830,6 +870,29 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 }
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
+
+// timeline of the profiled launches: out[3*i] = class, [3*i+1] = start ms,
+// [3*i+2] = end ms (relative to the first recorded event); returns the count
+int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
+    CtxLock lk(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    cudaDeviceSynchronize();
+    const auto& recs = ctx->prof.recs;
+    if (recs.empty()) return 0;
+    const cudaEvent_t base = recs[0].a;
+    int n = 0;
+    for (const auto& r : recs) {
+        if (n >= max_records) break;
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, base, r.a);
+        cudaEventElapsedTime(&b, base, r.b);
+        out[3 * n] = r.cls;
+        out[3 * n + 1] = a;
+        out[3 * n + 2] = b;
+        ++n;
+    }
+    return n;
+}
 
 int fl_debug_panel_profile(double* out8, int reset) {
     panel_profile(out8, reset != 0);

@@ -108,7 +108,10 @@ void panel_profile(double* out8, bool reset) {
 }
 
 template <int W, int ROWS, int NT>
-__global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
+// 256-thread variants are capped at 128 registers so a panel CTA fits on an SM
+// beside one DMMA GEMM CTA: the look-ahead panel then overlaps the trailing
+// update instead of waiting for a fully drained SM.
+__global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 : 1)
     panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char raw[];
@@ -373,12 +376,6 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
             }
             __syncthreads();
         }
-        if (rank == 0)
-            for (int e = tid; e < W * nrc; e += NT) {
-                const int i = e % W, c = e / W;
-                Fr[at(c0 + i, rc0 + c)] = sh.Ur[i][c];
-                Fi[at(c0 + i, rc0 + c)] = sh.Ui[i][c];
-            }
         PPROF(6);
         // ---- own rows >= rc0: A[row, rc0:] -= L[row, leaf] U
 #pragma unroll
@@ -411,7 +408,15 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT)
                     }
             }
         }
-        __syncthreads();
+        // every CTA has read T (rows c0..c0+W, right columns) before rank 0
+        // overwrites it with U: no CTA's later work touches those rows
+        cluster.sync();
+        if (rank == 0)
+            for (int e = tid; e < W * nrc; e += NT) {
+                const int i = e % W, c = e / W;
+                Fr[at(c0 + i, rc0 + c)] = sh.Ur[i][c];
+                Fi[at(c0 + i, rc0 + c)] = sh.Ui[i][c];
+            }
         PPROF(7);
     }
     // ---- rank 0: net permutation of all 64 interchanges for the outer laswp
@@ -439,9 +444,9 @@ void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cuda
     if (R <= 256)
         launch_reg<16, 1, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 512)
-        launch_reg<16, 1, 512>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<8, 2, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 1024)
-        launch_reg<8, 2, 512>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 4, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 2048)
         launch_reg<4, 4, 512>(F, N, k0, ipiv, ptab, batch, s);
     else

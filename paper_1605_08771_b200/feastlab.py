@@ -111,6 +111,7 @@ class Context:
 
     KERNEL_CLASSES = ("shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
                       "allreduce")
+    PHASE_CLASSES = ("eig", "orthonormalize", "rayleigh_ritz")
 
     def set_streams(self, n: int) -> None:
         """Contour-node chunks in flight (1 serialises the filter's kernels)."""

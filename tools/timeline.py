@@ -1,0 +1,44 @@
+# per-class busy time and overlap timeline of one filter application
+import ctypes, sys
+import numpy as np
+sys.path.insert(0, '.')
+import paper_1605_08771_b200 as P
+from paper_1605_08771_b200 import _lib
+n, p, nc = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+streams = int(sys.argv[4]) if len(sys.argv) > 4 else 4
+ctx = P.default_context()
+A = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n))); A = 0.5 * (A + A.T) / np.sqrt(n)
+X = np.asfortranarray(np.random.default_rng(1).standard_normal((n, p)))
+f = P.FilterApplier(A, P.build_contour_rule(P.SearchInterval(-0.3, 0.2), nc), ctx=ctx)
+ctx.set_streams(streams)
+f.apply(X)
+ctx.set_profiling(True)
+f.apply(X)
+buf = (ctypes.c_double * (3 * 200000))()
+cnt = _lib.lib().fl_ctx_profile_dump(ctx.handle, buf, 200000)
+ctx.set_profiling(False)
+rec = np.frombuffer(buf, dtype=np.float64, count=3 * cnt).reshape(-1, 3)
+names = ["shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate", "allreduce"]
+T = rec[:, 2].max()
+print(f"n={n} p={p} nc={nc} streams={streams}: span {T:.1f} ms, {cnt} records")
+# busy union per class and overall
+grid = np.linspace(0, T, 20001)
+busy = {}
+for ci, nm in enumerate(names):
+    r = rec[rec[:, 0] == ci]
+    if len(r) == 0: continue
+    act = np.zeros(len(grid), bool)
+    for a, b in r[:, 1:]:
+        act[(grid >= a) & (grid < b)] = True
+    busy[nm] = act
+    print(f"  {nm:10s} busy {100*act.mean():5.1f}% of span ({act.mean()*T:.1f} ms)")
+if "panel" in busy and "zgemm" in busy:
+    pn, gm = busy["panel"], busy["zgemm"]
+    print(f"  panel-only (no zgemm running) {100*(pn & ~gm).mean():.1f}%  ({(pn & ~gm).mean()*T:.1f} ms)")
+    anyb = np.zeros(len(grid), bool)
+    for v in busy.values(): anyb |= v
+    print(f"  idle {100*(~anyb).mean():.1f}%")
+# phase split of the span: factor vs solve (first permute start)
+perm = rec[rec[:, 0] == 5]
+if len(perm):
+    print(f"  first solve starts at {perm[:,1].min():.1f} ms, last at {perm[:,1].max():.1f} ms")
