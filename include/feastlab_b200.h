@@ -71,6 +71,9 @@ int fl_ctx_create(int device, fl_ctx** out, fl_err* err);
 int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl_ctx** out,
                        fl_err* err);
 int fl_nccl_unique_id(void* out128, fl_err* err);
+/* contour nodes owned by `rank` of `nranks`: [*k_begin, *k_end), contiguous,
+   ascending; the shards of all ranks partition [0, n_c) */
+int fl_node_shard(int n_c, int rank, int nranks, int* k_begin, int* k_end);
 int fl_ctx_destroy(fl_ctx* ctx);
 int fl_ctx_sync(fl_ctx* ctx, fl_err* err);
 void* fl_ctx_stream(fl_ctx* ctx); /* cudaStream_t */

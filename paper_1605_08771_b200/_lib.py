@@ -46,6 +46,7 @@ _SIGS = {
     "fl_ctx_create": (_I, [_I, _PP, _P]),
     "fl_ctx_create_nccl": (_I, [_I, _P, _I, _I, _PP, _P]),
     "fl_nccl_unique_id": (_I, [_P, _P]),
+    "fl_node_shard": (_I, [_I, _I, _I, _P, _P]),
     "fl_ctx_destroy": (_I, [_P]),
     "fl_ctx_sync": (_I, [_P, _P]),
     "fl_ctx_stream": (_P, [_P]),

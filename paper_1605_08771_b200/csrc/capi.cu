@@ -1074,9 +1074,7 @@ int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr,
         f->wi.assign(wi, wi + n_c);
         f->cache = cache != 0;
         // contiguous node shard of this rank
-        const int R = ctx->nranks, r = ctx->rank;
-        f->kb = (int)((long)n_c * r / R);
-        f->ke = (int)((long)n_c * (r + 1) / R);
+        fl_node_shard(n_c, ctx->rank, ctx->nranks, &f->kb, &f->ke);
         f->factored.assign(f->ke - f->kb, 0);
         *out = f.release();
     });

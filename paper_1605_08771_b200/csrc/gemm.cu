@@ -156,15 +156,24 @@ __global__ void __launch_bounds__(128) zgemm_kernel(ZGemm g) {
                 br[j] = frag<true>(br_s, wn + j * 8 + gq, kk + tq);
                 bi[j] = frag<true>(bi_s, wn + j * 8 + gq, kk + tq);
             }
+            // four passes over the 16 accumulator tiles: two DMMAs into the
+            // same accumulator are 32 instructions apart (no dependent stall)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    dmma(accr[i][j], ar[i], br[j]);
-                    dmma(acci[i][j], ar[i], bi[j]);
-                    dmma(accr[i][j], nai[i], bi[j]);
-                    dmma(acci[i][j], ai[i], br[j]);
-                }
+                for (int j = 0; j < 4; ++j) dmma(accr[i][j], ar[i], br[j]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acci[i][j], ar[i], bi[j]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(accr[i][j], nai[i], bi[j]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acci[i][j], ai[i], br[j]);
         }
         __syncthreads();
     }

@@ -181,3 +181,10 @@ void fl_uniform_fill(double* out, long long count, double lo, double hi, uint64_
 }
 
 }  // extern "C"
+
+extern "C" int fl_node_shard(int n_c, int rank, int nranks, int* k_begin, int* k_end) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || n_c < 0) return FL_INVALID_ARGUMENT;
+    *k_begin = static_cast<int>(static_cast<long long>(n_c) * rank / nranks);
+    *k_end = static_cast<int>(static_cast<long long>(n_c) * (rank + 1) / nranks);
+    return FL_OK;
+}

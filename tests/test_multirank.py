@@ -1,0 +1,81 @@
+"""N > 1 host path on CPU with gloo (world_size 2): node sharding, the
+rendezvous helpers of bench.py, and the sharded filter sum (each rank's
+ascending partial sum over its contiguous node shard, then a sum all-reduce)
+reproducing the single-process filter. The CUDA/NCCL data path itself needs
+GPUs (the round's GPU tier has one); its host logic is what runs here."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+
+        import oracle as O
+        from paper_1605_08771_b200 import dist as D
+        # rendezvous helpers
+        uid = bytes(range(128)) if rank == 0 else None
+        got = D.broadcast_bytes(uid, 128, 0)
+        assert got == bytes(range(128))
+        assert D.max_over_ranks(float(rank + 1)) == float(world)
+        # sharded filter: rank r sums its contiguous nodes in ascending order
+        n, p, nc = 40, 3, 8
+        A = O.random_symmetric(n, 77) / np.sqrt(n)
+        X = O.random_block(n, p, 78)
+        rule = O.build_contour_rule(O.SearchInterval(-0.5, 0.5), nc)
+        kb, ke = D.node_shard(nc, rank, world)
+        part = O.ContourRule(rule.interval, rule.nodes[kb:ke], rule.weights[kb:ke])
+        Y = O.apply_filter(A, part, X) if ke > kb else np.zeros((n, p))
+        t = torch.from_numpy(np.ascontiguousarray(Y))
+        dist.all_reduce(t)
+        if rank == 0:
+            full = O.apply_filter(A, rule, X)
+            out.put(("ok", float(np.linalg.norm(t.numpy() - full) / np.linalg.norm(full))))
+    except Exception as e:  # report to the parent
+        out.put(("err", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_node_shards_partition_the_rule():
+    from paper_1605_08771_b200 import dist as D
+    for nc in (1, 8, 16, 32, 5, 64):
+        for world in (1, 2, 4, 8):
+            covered = []
+            for r in range(world):
+                kb, ke = D.node_shard(nc, r, world)
+                assert 0 <= kb <= ke <= nc
+                covered.extend(range(kb, ke))
+            assert covered == list(range(nc))
+    with pytest.raises(ValueError):
+        D.node_shard(8, 2, 2)
+
+
+def test_two_rank_sharded_filter_sum_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+    status, val = q.get(timeout=10)
+    assert status == "ok", val
+    assert val <= 1e-13
