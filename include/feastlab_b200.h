@@ -89,6 +89,9 @@ int fl_ctx_set_streams(fl_ctx* ctx, int n);
 /* timeline of the profiled launches: out[3i] = class index (order of
    fl_ctx_profile's classes), out[3i+1] / out[3i+2] = start / end in ms */
 int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records);
+/* microbenchmark of the planar-complex DMMA GEMM (instrumentation) */
+int fl_debug_zgemm(fl_ctx* ctx, int M, int N, int K, int batch, int iters, double* ms_out,
+                   fl_err* err);
 /* cycle counts of the LU panel kernel's phases (instrumentation) */
 int fl_debug_panel_profile(double* out8, int reset);
 int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,

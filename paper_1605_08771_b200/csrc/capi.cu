@@ -282,49 +282,77 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
         launch_shift(f->A->d(), N, N, F, z, G, st);
     }
-    CK(cudaEventRecord(ev_next, st));  // shift done: panel 0 may start
-    for (int k0 = 0; k0 < N; k0 += FL_TILE) {
-        {
-            CK(cudaStreamWaitEvent(sp, ev_next, 0));
-            Prof pr(ctx, P_PANEL, 0.0, 2, sp);
-            launch_panel(F, N, k0, ipiv, ptab, G, sp);
-            launch_trinv(F, k0, 1, false, Inv, k0 / FL_TILE, G, sp);
+    const int T = FL_TILE;
+    auto E = [&](int r, int c) { return (long)c * N + r; };
+    // C[r,c: +M x +nc] -= A[ar,ac: M x K] B[br,bc: K x nc]
+    auto sub = [&](int M, int nc, int K, int ar, int ac, int br, int bc, int cr, int cc,
+                   cudaStream_t s) {
+        if (M <= 0 || nc <= 0) return;
+        ZGemm g{M, nc, K, F.re + E(ar, ac), F.im + E(ar, ac), N, stride,
+                F.re + E(br, bc), F.im + E(br, bc), N, stride,
+                F.re + E(cr, cc), F.im + E(cr, cc), N, stride};
+        Prof pr(ctx, P_ZGEMM, 8.0 * M * nc * K * G, 1, s);
+        launch_zgemm_sub(g, G, s);
+    };
+    // F[k:k+64, c:c+nc] = L_kk^{-1} F[k:k+64, c:c+nc] (in place)
+    auto linv = [&](int k, int c, int nc, cudaStream_t s) {
+        if (nc <= 0) return;
+        const long ib = (long)(k / T) * T * T;
+        ZGemm u{T, nc, T, Inv.re + ib, Inv.im + ib, T, Inv.stride,
+                F.re + E(k, c), F.im + E(k, c), N, stride, F.re + E(k, c), F.im + E(k, c), N,
+                stride};
+        Prof pr(ctx, P_TRSM, 8.0 * T * T * nc * G, 1, s);
+        launch_zgemm_set(u, G, s);
+    };
+    // two pivot tables: panel B's must not overwrite panel A's before st uses it
+    int* tabs[2] = {ptab, f->ptab.i() + (long)(f->fac_slots + s0) * (4 * T + 1)};
+    auto panel = [&](int k, int* tab) {
+        Prof pr(ctx, P_PANEL, 0.0, 2, sp);
+        launch_panel(F, N, k, ipiv, tab, G, sp);
+        launch_trinv(F, k, 1, false, Inv, k / T, G, sp);
+    };
+    auto swaps = [&](const int* tab, int a0, int a1, int b0, int b1, cudaStream_t s) {
+        Prof pr(ctx, P_LASWP, 0.0, 1, s);
+        launch_laswp(F, a0, a1, b0, b1, tab, G, s);
+    };
+    // Outer blocks of 128 columns = panels A (kA) and B (kB = kA + 64). The
+    // panel stream factors BOTH panels while the main stream finishes the
+    // previous block's trailing update (look-ahead); the trailing update then
+    // has K = 128 (half the C-tile traffic of K = 64):
+    //   sp: panel A | A-swaps on B's columns | U_A[:, B] = L_AA^-1 (.) |
+    //       A[kB:, B] -= L_A U_A[:, B] | panel B                       -> ev_panel
+    //   st: A-swaps, B-swaps on the other columns | U_A[:, rest] |
+    //       A[kB, rest] -= L_A[kB,:] U_A[:, rest] | U_B = L_BB^-1 (.) |
+    //       A[kB+64:, rest] -= [L_A L_B] [U_A; U_B]  (next block's 128 columns
+    //       first -> ev_next, then the remainder)
+    CK(cudaEventRecord(ev_next, st));  // shift done: block 0 may start
+    for (int kA = 0; kA < N; kA += 2 * T) {
+        const int kB = kA + T, c0 = kB + T;
+        CK(cudaStreamWaitEvent(sp, ev_next, 0));
+        panel(kA, tabs[0]);
+        if (kB < N) {
+            swaps(tabs[0], kB, kB + T, 0, 0, sp);
+            linv(kA, kB, T, sp);
+            sub(N - kB, T, T, kB, kA, kA, kB, kB, kB, sp);
+            panel(kB, tabs[1]);
         }
         CK(cudaEventRecord(ev_panel, sp));
         CK(cudaStreamWaitEvent(st, ev_panel, 0));
-        {
-            Prof pr(ctx, P_LASWP, 0.0, 1, st);
-            launch_laswp_panel(F, N, k0, ptab, G, st);
+        if (kB >= N) {
+            swaps(tabs[0], 0, kA, 0, 0, st);
+            break;
         }
-        const int rest = N - k0 - FL_TILE;
-        if (rest > 0) {
-            {
-                // U12 = L11^{-1} A12, in place
-                Prof pr(ctx, P_TRSM, 8.0 * FL_TILE * FL_TILE * rest * G, 1, st);
-                ZGemm u{FL_TILE, rest, FL_TILE,
-                        Inv.re + (long)(k0 / FL_TILE) * FL_TILE * FL_TILE,
-                        Inv.im + (long)(k0 / FL_TILE) * FL_TILE * FL_TILE, FL_TILE, Inv.stride,
-                        F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0,
-                        N, stride,
-                        F.re + (long)(k0 + FL_TILE) * N + k0, F.im + (long)(k0 + FL_TILE) * N + k0,
-                        N, stride};
-                launch_zgemm_set(u, G, st);
-            }
-            // trailing update A22 -= L21 U12, split: next panel's columns first
-            auto upd = [&](int c0, int nc) {
-                ZGemm g{rest, nc, FL_TILE,
-                        F.re + (long)k0 * N + k0 + FL_TILE, F.im + (long)k0 * N + k0 + FL_TILE, N,
-                        stride,
-                        F.re + (long)c0 * N + k0, F.im + (long)c0 * N + k0, N, stride,
-                        F.re + (long)c0 * N + k0 + FL_TILE, F.im + (long)c0 * N + k0 + FL_TILE, N,
-                        stride};
-                Prof pr(ctx, P_ZGEMM, 8.0 * rest * nc * FL_TILE * G, 1, st);
-                launch_zgemm_sub(g, G, st);
-            };
-            upd(k0 + FL_TILE, FL_TILE);
-            CK(cudaEventRecord(ev_next, st));
-            if (rest > FL_TILE) upd(k0 + 2 * FL_TILE, rest - FL_TILE);
-        }
+        swaps(tabs[0], 0, kA, c0, N, st);
+        swaps(tabs[1], 0, kB, c0, N, st);
+        const int rest = N - c0;
+        if (rest <= 0) break;
+        linv(kA, c0, rest, st);
+        sub(T, rest, T, kB, kA, kA, c0, kB, c0, st);
+        linv(kB, c0, rest, st);
+        const int nxt = std::min(2 * T, rest);
+        sub(rest, nxt, 2 * T, c0, kA, kA, c0, c0, c0, st);
+        CK(cudaEventRecord(ev_next, st));
+        sub(rest, rest - nxt, 2 * T, c0, kA, kA, c0 + nxt, c0, c0 + nxt, st);
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
@@ -420,7 +448,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->fac_im.ensure(sizeof(double) * (size_t)fstride * slots);
         f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
         f->perm.ensure(sizeof(int) * (size_t)N * slots);
-        f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * slots);
+        f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * 2 * slots);
         f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->fac_slots = slots;
@@ -892,6 +920,38 @@ int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
         ++n;
     }
     return n;
+}
+
+// microbenchmark of the planar-complex DMMA GEMM (C -= A B, batch x M x N x K,
+// operands resident in HBM): average milliseconds per launch
+int fl_debug_zgemm(fl_ctx* ctx, int M, int Nc, int K, int batch, int iters, double* ms_out,
+                   fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        if (M % 64 || Nc % 64 || K % 16 || batch < 1 || iters < 1)
+            throw Fail{FL_INVALID_ARGUMENT, "fl_debug_zgemm: bad shape"};
+        const size_t a = (size_t)M * K, b = (size_t)K * Nc, c = (size_t)M * Nc;
+        DBuf buf;
+        buf.ensure(sizeof(double) * 2 * (a + b + c) * batch);
+        CK(cudaMemsetAsync(buf.p, 0, sizeof(double) * 2 * (a + b + c) * batch, ctx->stream));
+        double* base = buf.d();
+        const long sa = 2 * a, sb = 2 * b, sc = 2 * c;
+        ZGemm g{M, Nc, K, base, base + a, M, sa, base + sa * batch, base + sa * batch + b, K, sb,
+                base + (sa + sb) * batch, base + (sa + sb) * batch + c, M, sc};
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        launch_zgemm_sub(g, batch, ctx->stream);
+        cudaEventRecord(e0, ctx->stream);
+        for (int i = 0; i < iters; ++i) launch_zgemm_sub(g, batch, ctx->stream);
+        cudaEventRecord(e1, ctx->stream);
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms / iters;
+    });
 }
 
 int fl_debug_panel_profile(double* out8, int reset) {

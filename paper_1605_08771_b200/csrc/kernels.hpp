@@ -53,8 +53,9 @@ void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& 
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s);
 // Cycle counts of the panel kernel phases (node 0, rank 0, thread 0).
 void panel_profile(double* out8, bool reset);
-// Apply the panel's 64 row interchanges (ptab) to all columns outside the panel.
-void launch_laswp_panel(ZBatch F, int N, int k0, const int* ptab, int batch, cudaStream_t s);
+// Apply a panel's 64 row interchanges (ptab) to the columns [a0,a1) U [b0,b1).
+void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int batch,
+                  cudaStream_t s);
 // Inverses of `nblocks` consecutive 64x64 diagonal blocks starting at (r0, r0):
 // unit-lower (upper=false) or upper. Block j of node b is stored at
 // Inv.re/im + b*Inv.stride + (first_block + j)*4096, column-major ld 64.

@@ -70,8 +70,8 @@ constexpr int PW = 64;
 // gather/scatter of the <= 128 moved rows (net permutation from the panel
 // kernel): every load of a CTA is issued before any store.
 constexpr int LS_COLS = 16;
-__global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int N, int k0,
-                                                          const int* __restrict__ ptab) {
+__global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int a0, int a1, int b0,
+                                                          int b1, const int* __restrict__ ptab) {
     __shared__ double vr[2 * PW][LS_COLS + 1];
     __shared__ double vi[2 * PW][LS_COLS + 1];
     __shared__ int pos[2 * PW], src[2 * PW];
@@ -83,15 +83,15 @@ __global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int N, int k
         src[m] = tab[1 + 2 * PW + m];
     }
     __syncthreads();
-    const int ncols = N - PW;
+    const int na = a1 - a0, ncols = na + (b1 - b0);
     double* Fr = F.re + b * F.stride;
     double* Fi = F.im + b * F.stride;
     const int c0 = blockIdx.x * LS_COLS;
     for (int e = threadIdx.x; e < cnt * LS_COLS; e += blockDim.x) {
         const int m = e % cnt, c = e / cnt;
-        int col = c0 + c;
-        if (col >= ncols) continue;
-        if (col >= k0) col += PW;
+        const int k = c0 + c;
+        if (k >= ncols) continue;
+        const int col = k < na ? a0 + k : b0 + (k - na);
         const long o = (long)col * F.ld + src[m];
         vr[m][c] = Fr[o];
         vi[m][c] = Fi[o];
@@ -99,19 +99,23 @@ __global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int N, int k
     __syncthreads();
     for (int e = threadIdx.x; e < cnt * LS_COLS; e += blockDim.x) {
         const int m = e % cnt, c = e / cnt;
-        int col = c0 + c;
-        if (col >= ncols) continue;
-        if (col >= k0) col += PW;
+        const int k = c0 + c;
+        if (k >= ncols) continue;
+        const int col = k < na ? a0 + k : b0 + (k - na);
         const long o = (long)col * F.ld + pos[m];
         Fr[o] = vr[m][c];
         Fi[o] = vi[m][c];
     }
 }
 
-void launch_laswp_panel(ZBatch F, int N, int k0, const int* ptab, int batch, cudaStream_t s) {
-    const int ncols = N - PW;
+void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int batch,
+                  cudaStream_t s) {
+    a1 = a1 > a0 ? a1 : a0;
+    b1 = b1 > b0 ? b1 : b0;
+    const int ncols = (a1 - a0) + (b1 - b0);
     if (ncols <= 0) return;
-    laswp_panel_kernel<<<dim3((ncols + LS_COLS - 1) / LS_COLS, batch), 256, 0, s>>>(F, N, k0, ptab);
+    laswp_panel_kernel<<<dim3((ncols + LS_COLS - 1) / LS_COLS, batch), 256, 0, s>>>(F, a0, a1, b0,
+                                                                                   b1, ptab);
 }
 
 // ------------------------------------------------------------------ 64x64 triangular inverses
