@@ -383,30 +383,35 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
                 W.re + r0, W.im + r0, N, W.stride, W.re + r0, W.im + r0, N, W.stride};
         launch_zgemm_set(u, G, st);
     };
-    for (int ib = 0; ib < NB; ++ib) {  // forward, unit lower
-        const int r0 = ib * FL_TILE;
+    // W[wr: +M] -= F[fr: +M, fc: +K] W[wk: +K]
+    auto sub = [&](int M, int K, int fr, int fc, int wk, int wr) {
+        if (M <= 0) return;
+        ZGemm g{M, P, K, F.re + (long)fc * N + fr, F.im + (long)fc * N + fr, N, stride,
+                W.re + wk, W.im + wk, N, W.stride, W.re + wr, W.im + wr, N, W.stride};
+        Prof pr(ctx, P_ZGEMM, 8.0 * M * P * K * G, 1, st);
+        launch_zgemm_sub(g, G, st);
+    };
+    // 128-row steps, so the long updates have K = 128 (cf. the LU):
+    // forward (unit lower): W_i = L_ii^-1 W_i; W_{i+1} -= L_{i+1,i} W_i;
+    //   W_{i+1} = L^-1 W_{i+1}; W_{i+2:} -= L_{i+2:, i:i+2} W_{i:i+2}
+    const int T = FL_TILE;
+    for (int ib = 0; ib < NB; ib += 2) {
+        const int r0 = ib * T;
         tri(ib, r0);
-        const int rest = N - r0 - FL_TILE;
-        if (rest > 0) {
-            ZGemm g{rest, P, FL_TILE,
-                    F.re + (long)r0 * N + r0 + FL_TILE, F.im + (long)r0 * N + r0 + FL_TILE, N, stride,
-                    W.re + r0, W.im + r0, N, W.stride,
-                    W.re + r0 + FL_TILE, W.im + r0 + FL_TILE, N, W.stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * rest * P * FL_TILE * G, 1, st);
-            launch_zgemm_sub(g, G, st);
-        }
+        if (ib + 1 >= NB) break;
+        sub(T, T, r0 + T, r0, r0, r0 + T);
+        tri(ib + 1, r0 + T);
+        sub(N - r0 - 2 * T, 2 * T, r0 + 2 * T, r0, r0, r0 + 2 * T);
     }
-    for (int ib = NB - 1; ib >= 0; --ib) {  // backward, upper
-        const int r0 = ib * FL_TILE;
-        tri(NB + ib, r0);
-        if (r0 > 0) {
-            ZGemm g{r0, P, FL_TILE,
-                    F.re + (long)r0 * N, F.im + (long)r0 * N, N, stride,
-                    W.re + r0, W.im + r0, N, W.stride,
-                    W.re, W.im, N, W.stride};
-            Prof pr(ctx, P_ZGEMM, 8.0 * r0 * P * FL_TILE * G, 1, st);
-            launch_zgemm_sub(g, G, st);
-        }
+    // backward (upper), from the bottom in 128-row steps aligned to the end
+    for (int ib = NB - 1; ib >= 0; ib -= 2) {
+        const int r1 = ib * T;  // lower block of the pair
+        tri(NB + ib, r1);
+        if (ib == 0) break;
+        const int r0 = r1 - T;
+        sub(T, T, r0, r1, r1, r0);
+        tri(NB + ib - 1, r0);
+        sub(r0, 2 * T, 0, r0, r0, 0);
     }
 }
 
@@ -518,7 +523,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             throw fl;
         }
     }
-    if (f->cache && ctx->nranks > 1) {
+    if (f->cache && ctx->comm) {
         // factorizations are counted globally: every rank adds the same total
         long long loc = new_facts, tot = 0;
         DBuf t;
@@ -543,7 +548,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     } else {
         CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
     }
-    if (ctx->nranks > 1) {
+    if (ctx->comm) {
         if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
         Prof pr(ctx, P_ALLREDUCE, 8.0 * N * p, 0);
         nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm, ctx->stream),
@@ -831,7 +836,7 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         c->rank = rank;
         c->nranks = nranks;
-        if (nranks > 1) {
+        if (id != nullptr) {  // a clique (also of one rank: exercises the NCCL path)
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof(uid));
             nccl_check(ncclCommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
@@ -847,8 +852,8 @@ int fl_ctx_create(int device, fl_ctx** out, fl_err* err) {
 
 int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl_ctx** out,
                        fl_err* err) {
-    if (nranks < 1 || rank < 0 || rank >= nranks)
-        return report(err, Fail{FL_INVALID_ARGUMENT, "bad rank/nranks"});
+    if (nranks < 1 || rank < 0 || rank >= nranks || nccl_id == nullptr)
+        return report(err, Fail{FL_INVALID_ARGUMENT, "bad rank/nranks or missing NCCL id"});
     return ctx_create_impl(device, nccl_id, rank, nranks, out, err);
 }
 

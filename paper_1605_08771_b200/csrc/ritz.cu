@@ -5,6 +5,8 @@
 // gather streams.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ritz_kernels.hpp"
 
@@ -327,81 +329,136 @@ __global__ void __launch_bounds__(256) jacobi_kernel(JacobiArgs J) {
         return M[(long)j * lda + i];
     };
     int sweep = 0;
+    const long gthreads = (long)gridDim.x * blockDim.x;
+    const long gtid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long nblk = (long)half * (half + 1) / 2;
+    const long nv = (long)p * half;
+    // each phase below issues all of a thread's loads before using any of them,
+    // so a round costs one L2 round trip per phase plus the grid barrier
+    constexpr int BATCH = 4;
     for (; sweep < J.max_sweeps; ++sweep) {
         for (int r = 0; r < pe - 1; ++r) {
             if (threadIdx.x == 0) cnt = 0;
             __syncthreads();
-            // rotations of this round (every CTA, redundantly)
+            // rotations of this round (every CTA, redundantly; half <= 4 * 256)
             unsigned long long local = 0;
-            for (int k = threadIdx.x; k < half; k += blockDim.x) {
-                int a, b;
-                round_pair(r, k, pe, a, b);
-                pa[k] = a;
-                pb[k] = b;
-                role[a] = 2 * k;
-                role[b] = 2 * k + 1;
-                double c = 1.0, s = 0.0, t = 0.0;
-                if (b < p) {
-                    const double apq = el(Acur, a, b);
-                    if (fabs(apq) > J.thr) {
-                        const double app = el(Acur, a, a), aqq = el(Acur, b, b);
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                        ++local;
+            {
+                int ka[BATCH], kb_[BATCH];
+                double apq[BATCH], app[BATCH], aqq[BATCH];
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const int k = threadIdx.x + u * blockDim.x;
+                    ka[u] = -1;
+                    kb_[u] = -1;
+                    if (k < half) {
+                        round_pair(r, k, pe, ka[u], kb_[u]);
+                        const bool ok = kb_[u] < p;
+                        apq[u] = ok ? Acur[(long)kb_[u] * lda + ka[u]] : 0.0;
+                        app[u] = ok ? Acur[(long)ka[u] * lda + ka[u]] : 0.0;
+                        aqq[u] = ok ? Acur[(long)kb_[u] * lda + kb_[u]] : 0.0;
                     }
                 }
-                cs[k] = c;
-                sn[k] = s;
-                tt[k] = t;
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const int k = threadIdx.x + u * blockDim.x;
+                    if (k >= half) continue;
+                    pa[k] = ka[u];
+                    pb[k] = kb_[u];
+                    double c = 1.0, sn_ = 0.0, t = 0.0;
+                    if (kb_[u] < p && fabs(apq[u]) > J.thr) {
+                        const double tau = (aqq[u] - app[u]) / (2.0 * apq[u]);
+                        t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        sn_ = t * c;
+                        ++local;
+                    }
+                    cs[k] = c;
+                    sn[k] = sn_;
+                    tt[k] = t;
+                }
             }
             if (local) atomicAdd(&cnt, local);
             __syncthreads();
             if (blockIdx.x == 0 && threadIdx.x == 0 && cnt) atomicAdd(&J.rot_count[sweep], cnt);
-            // apply: blocks (P, Q) of 2x2, all P, Q in [0, half)
-            const long nblk = (long)half * half;
-            for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nblk;
-                 e += (long)gridDim.x * blockDim.x) {
-                const int P = (int)(e % half), Q = (int)(e / half);
-                const int a1 = pa[P], b1 = pb[P], a2 = pa[Q], b2 = pb[Q];
-                const double c1 = cs[P], s1 = sn[P], c2 = cs[Q], s2 = sn[Q];
-                const double Baa = el(Acur, a1, a2), Bab = el(Acur, a1, b2);
-                const double Bba = el(Acur, b1, a2), Bbb = el(Acur, b1, b2);
-                double naa, nab, nba, nbb;
-                if (P == Q && s1 != 0.0) {
-                    const double t = tt[P];
-                    naa = Baa - t * Bab;
-                    nbb = Bbb + t * Bab;
-                    nab = 0.0;
-                    nba = 0.0;
-                } else {
-                    // rows: x_a = c1*row_a - s1*row_b ; x_b = s1*row_a + c1*row_b
-                    const double ra_a = c1 * Baa - s1 * Bba, ra_b = c1 * Bab - s1 * Bbb;
-                    const double rb_a = s1 * Baa + c1 * Bba, rb_b = s1 * Bab + c1 * Bbb;
-                    naa = ra_a * c2 - ra_b * s2;
-                    nab = ra_a * s2 + ra_b * c2;
-                    nba = rb_a * c2 - rb_b * s2;
-                    nbb = rb_a * s2 + rb_b * c2;
+            // apply: 2x2 blocks (P, Q), P <= Q only (A' symmetric: also written
+            // transposed); V' = V J on column pairs
+            for (long e0 = gtid; e0 < nblk; e0 += BATCH * gthreads) {
+                double B[BATCH][4];
+                int PQ[BATCH][2];
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const long e = e0 + u * gthreads;
+                    PQ[u][0] = -1;
+                    if (e >= nblk) continue;
+                    int Q = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+                    while ((long)Q * (Q + 1) / 2 > e) --Q;
+                    while ((long)(Q + 1) * (Q + 2) / 2 <= e) ++Q;
+                    const int P = (int)(e - (long)Q * (Q + 1) / 2);
+                    PQ[u][0] = P;
+                    PQ[u][1] = Q;
+                    B[u][0] = el(Acur, pa[P], pa[Q]);
+                    B[u][1] = el(Acur, pa[P], pb[Q]);
+                    B[u][2] = el(Acur, pb[P], pa[Q]);
+                    B[u][3] = el(Acur, pb[P], pb[Q]);
                 }
-                if (a1 < p && a2 < p) Anext[(long)a2 * lda + a1] = naa;
-                if (a1 < p && b2 < p) Anext[(long)b2 * lda + a1] = nab;
-                if (b1 < p && a2 < p) Anext[(long)a2 * lda + b1] = nba;
-                if (b1 < p && b2 < p) Anext[(long)b2 * lda + b1] = nbb;
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const int P = PQ[u][0], Q = PQ[u][1];
+                    if (P < 0) continue;
+                    const int a1 = pa[P], b1 = pb[P], a2 = pa[Q], b2 = pb[Q];
+                    const double c1 = cs[P], s1 = sn[P], c2 = cs[Q], s2 = sn[Q];
+                    const double Baa = B[u][0], Bab = B[u][1], Bba = B[u][2], Bbb = B[u][3];
+                    double naa, nab, nba, nbb;
+                    if (P == Q && s1 != 0.0) {
+                        const double t = tt[P];
+                        naa = Baa - t * Bab;
+                        nbb = Bbb + t * Bab;
+                        nab = 0.0;
+                        nba = 0.0;
+                    } else {
+                        // rows: x_a = c1*row_a - s1*row_b ; x_b = s1*row_a + c1*row_b
+                        const double ra_a = c1 * Baa - s1 * Bba, ra_b = c1 * Bab - s1 * Bbb;
+                        const double rb_a = s1 * Baa + c1 * Bba, rb_b = s1 * Bab + c1 * Bbb;
+                        naa = ra_a * c2 - ra_b * s2;
+                        nab = ra_a * s2 + ra_b * c2;
+                        nba = rb_a * c2 - rb_b * s2;
+                        nbb = rb_a * s2 + rb_b * c2;
+                    }
+                    if (a1 < p && a2 < p) Anext[(long)a2 * lda + a1] = naa;
+                    if (a1 < p && b2 < p) Anext[(long)b2 * lda + a1] = nab;
+                    if (b1 < p && a2 < p) Anext[(long)a2 * lda + b1] = nba;
+                    if (b1 < p && b2 < p) Anext[(long)b2 * lda + b1] = nbb;
+                    if (P != Q) {
+                        if (a1 < p && a2 < p) Anext[(long)a1 * lda + a2] = naa;
+                        if (a1 < p && b2 < p) Anext[(long)a1 * lda + b2] = nab;
+                        if (b1 < p && a2 < p) Anext[(long)b1 * lda + a2] = nba;
+                        if (b1 < p && b2 < p) Anext[(long)b1 * lda + b2] = nbb;
+                    }
+                }
             }
-            // V' = V J on column pairs
-            const long nv = (long)p * half;
-            for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nv;
-                 e += (long)gridDim.x * blockDim.x) {
-                const int x = (int)(e % p), P = (int)(e / p);
-                const double s1 = sn[P];
-                if (s1 == 0.0) continue;
-                const int a = pa[P], b = pb[P];
-                if (b >= p) continue;
-                const double c1 = cs[P];
-                const double va = J.V[(long)a * J.ldv + x], vb = J.V[(long)b * J.ldv + x];
-                J.V[(long)a * J.ldv + x] = c1 * va - s1 * vb;
-                J.V[(long)b * J.ldv + x] = s1 * va + c1 * vb;
+            for (long e0 = gtid; e0 < nv; e0 += BATCH * gthreads) {
+                double va[BATCH], vb[BATCH];
+                int xs[BATCH], Ps[BATCH];
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const long e = e0 + u * gthreads;
+                    Ps[u] = -1;
+                    if (e >= nv) continue;
+                    const int x = (int)(e % p), P = (int)(e / p);
+                    if (sn[P] == 0.0 || pb[P] >= p) continue;
+                    Ps[u] = P;
+                    xs[u] = x;
+                    va[u] = J.V[(long)pa[P] * J.ldv + x];
+                    vb[u] = J.V[(long)pb[P] * J.ldv + x];
+                }
+#pragma unroll
+                for (int u = 0; u < BATCH; ++u) {
+                    const int P = Ps[u];
+                    if (P < 0) continue;
+                    const double c1 = cs[P], s1 = sn[P];
+                    J.V[(long)pa[P] * J.ldv + xs[u]] = c1 * va[u] - s1 * vb[u];
+                    J.V[(long)pb[P] * J.ldv + xs[u]] = s1 * va[u] + c1 * vb[u];
+                }
             }
             grid.sync();
             double* t = Acur;
@@ -520,6 +577,10 @@ int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, 
     if (work_items < (long)blocks * 256) {
         blocks = (int)((work_items + 255) / 256);
         if (blocks < 1) blocks = 1;
+    }
+    if (const char* e = getenv("FL_JACOBI_BLOCKS")) {
+        const int want = atoi(e);
+        if (want > 0 && want < blocks) blocks = want;
     }
     void* args[] = {&J};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(blocks), dim3(256),

@@ -83,7 +83,7 @@ class Context:
     def __init__(self, device: int = 0, *, nccl_id: bytes | None = None, rank: int = 0,
                  nranks: int = 1):
         h = C.c_void_p()
-        if nranks > 1:
+        if nccl_id is not None:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _call(L.lib().fl_ctx_create_nccl, device, buf, rank, nranks, C.byref(h))
         else:

@@ -1,0 +1,33 @@
+"""Generate tests/golden/oracle_cfg<k>.json: the CPU oracle's FEAST / XFEAST /
+RFEAST results (traces, iteration/converged counts, eigenvalues) on a BASELINE
+configuration, so the GPU parity tests need not rerun minutes of CPU work.
+Usage: python tools/gen_golden.py <cfg> [threads]   (run in the build container)"""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle as O
+from paper_1605_08771_b200 import configs as CF
+
+idx = int(sys.argv[1])
+if len(sys.argv) > 2:
+    O.set_threads(int(sys.argv[2]))
+vals = CF.spectrum(idx, O.uniform_fill)
+c = CF.resolved(idx, vals)
+A = CF.laplacian_2d() if idx == 3 else O.assemble_matrix(vals, O.seeded_orthogonal(len(vals), 1000 + idx))
+out = {"cfg": idx, "config": c, "oracle_threads": O.get_threads(), "generator": "tools/gen_golden.py",
+       "drivers": {}}
+for d in ("feast_solve", "xfeast_solve", "rfeast_solve"):
+    t = time.time()
+    s = getattr(O, d)(A, O.SearchInterval(c["lo"], c["hi"]),
+                      O.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"], s=c["s"]))
+    out["drivers"][d] = {
+        "seconds": round(time.time() - t, 2), "iterations": s.iterations, "converged": s.converged,
+        "m": len(s.eigenvalues), "eigenvalues": [float(x) for x in s.eigenvalues],
+        "residual_norms": [float(x) for x in s.residual_norms], "recovery_events": s.recovery_events,
+        "rhs_solved": s.accounting.rhs_solved, "factorizations": s.accounting.factorizations,
+        "trace": [[t.iter, t.subspace_dim, t.rhs_cumulative, t.max_residual, t.m_found] for t in s.trace]}
+    print(d, out["drivers"][d]["iterations"], out["drivers"][d]["converged"], flush=True)
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                    f"oracle_cfg{idx}.json")
+with open(path, "w") as f:
+    json.dump(out, f)
+print("wrote", path)
