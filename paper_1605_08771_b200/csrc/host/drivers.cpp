@@ -5,7 +5,9 @@
 #include "feastlab/drivers.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <numeric>
 #include <ostream>
@@ -32,6 +34,29 @@ void write_trace_csv(std::ostream& os, const ConvergenceTrace& trace) {
 }
 
 namespace {
+
+// FEASTLAB_TIME=1: per-phase wall time of the feast_solve loop on stderr
+// (the context is synchronised at each phase boundary)
+struct PhaseTimer {
+    bool on = std::getenv("FEASTLAB_TIME") != nullptr;
+    fl_ctx* ctx;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double filter = 0, orth = 0, rr = 0, host = 0;
+    explicit PhaseTimer(fl_ctx* c) : ctx(c) {}
+    void lap(double& acc) {
+        if (!on) return;
+        fl_err e{};
+        fl_ctx_sync(ctx, &e);
+        const auto t = std::chrono::steady_clock::now();
+        acc += std::chrono::duration<double>(t - t0).count();
+        t0 = t;
+    }
+    ~PhaseTimer() {
+        if (on)
+            std::fprintf(stderr, "feast_solve phases [s]: filter %.3f orthonormalize %.3f "
+                                 "rayleigh_ritz %.3f host %.3f\n", filter, orth, rr, host);
+    }
+};
 
 // Ritz pairs with the vectors left on the device
 struct DevRitz {
@@ -169,20 +194,26 @@ Solution feast_solve(const SymmetricMatrix& A, const SearchInterval& interval,
     DeviceBlock Y(ctx, n, config.m0), U(ctx, n, config.m0);
     DevRitz rr(ctx, n);
     int last_m_found = 0;
+    PhaseTimer timer(ctx);
     for (int iter = 1; iter <= config.max_iter; ++iter) {
+        timer.lap(timer.host);
         filt.apply(X, Y, sol.accounting);
+        timer.lap(timer.filter);
         if (iter == 1 && detail::keep_first_filtered) sol.first_filtered = Y.download();
         int dim;
         if (config.generalized_reduced) {
             rr_device(ctx, filt.device_matrix(), Y, interval, rr);
             dim = Y.cols();
+            timer.lap(timer.rr);
         } else {
             const int rank = orth_device(ctx, Y, config, U);
+            timer.lap(timer.orth);
             if (rank < last_m_found)
                 throw std::runtime_error(
                     "feast_solve: filtered subspace rank collapsed below the inside "
                     "eigenpair count; m0 may be too small");
             rr_device(ctx, filt.device_matrix(), U, interval, rr);
+            timer.lap(timer.rr);
             dim = rank;
         }
         const std::vector<int> inside = inside_by_residual(rr);
