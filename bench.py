@@ -17,12 +17,11 @@ reference itself needs Eigen, which is absent) on the host cores.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -63,54 +62,74 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle-reason samples taken DURING the timed region.
+
+    In-process NVML polled from a thread every 50 ms (an `nvidia-smi -lms`
+    child contends for the driver with the launching thread and visibly
+    perturbed the launch-bound filter step). No NVML: "clocks" is null.
+    """
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.samples = []
+        self.reason_bits = 0
+        self.max_mhz = 0.0
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.device)
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:
+            self._nvml = None
+            return
+        self._nvml = nv
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    self.reason_bits |= int(get_reasons(h))
+                except Exception:
+                    pass
+                self._stop.wait(0.05)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
 
     def stop(self):
-        if not self.proc:
+        if self._thread is None:
             return None
-        self.proc.terminate()
+        self._stop.set()
+        self._thread.join()
         try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        os.unlink(self.path)
+            self._nvml.nvmlShutdown()
+        except Exception:
+            pass
+        sm = self.samples
         if not sm:
             return None
-        under = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(under), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        under = [x for x in sm if x > 0.5 * self.max_mhz] or sm
+        return {"sm_mhz": statistics.median(under), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.REASONS.items() if self.reason_bits & k),
+                "samples": len(sm), "source": "NVML (in-process, 50 ms)"}
 
 
 # ------------------------------------------------------------------ workload
@@ -239,6 +258,10 @@ def run_b200(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     ctx.sync()
+    # the launching thread must not pause inside the timed region: move the
+    # set-up objects out of the collector's reach (host-side only)
+    gc.collect()
+    gc.freeze()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -314,6 +337,7 @@ def run_b200(args, rank, world, local_rank):
 
     if rank != 0:
         return
+    mode = P.zgemm_mode()
     zms, zflops, zl = prof["zgemm"]
     total_ms_prof = sum(v[0] for v in prof.values())
     achieved = zflops / (zms * 1e-3) / 1e12 if zms > 0 else 0.0
@@ -337,8 +361,14 @@ def run_b200(args, rank, world, local_rank):
                    "parallelism": f"contour nodes sharded {nc}/{world} per GPU + NCCL allreduce",
                    "l2": "inputs larger than L2 (n_c LU factors, 16 n^2 B each)"},
         "fraction_of_fp64_peak": round(value / 1e3 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
-        "roofline": {"kernel": "zgemm_kernel (DMMA; LU trailing update, U12 and blocked solves)",
+        "roofline": {"kernel": f"zgemm{'3m' if mode == '3m' else ''}_kernel (DMMA; LU trailing "
+                               "update, U12 and blocked solves)",
                      "bound": "tensor", "achieved": round(achieved, 3),
+                     "product_form": mode,
+                     "flop_convention": "algorithmic 8MNK per complex GEMM (both forms); the 3M "
+                                        "form issues 6MNK on the DMMA pipe",
+                     "tensor_pipe_frac": round(achieved * (0.75 if mode == "3m" else 1.0)
+                                               / FP64_DMMA_PEAK_TFLOPS, 4),
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": None,

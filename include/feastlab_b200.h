@@ -86,8 +86,14 @@ long long fl_ctx_launches(const fl_ctx* ctx);
 int fl_ctx_set_profiling(fl_ctx* ctx, int on);
 /* number of contour-node chunks factored/solved concurrently (1..4, default 4) */
 int fl_ctx_set_streams(fl_ctx* ctx, int n);
-/* timeline of the profiled launches: out[3i] = class index (order of
-   fl_ctx_profile's classes), out[3i+1] / out[3i+2] = start / end in ms */
+/* complex product form of the filter's DMMA GEMMs (process-wide): 1 = 3M
+   (three real products per complex product, the default), 0 = 4M; mode < 0
+   only queries. Returns the mode in effect. Env FEASTLAB_ZGEMM=4m|3m sets
+   the initial value. */
+int fl_zgemm_mode(int mode);
+/* timeline of the profiled launches: out[4i] = class index (order of
+   fl_ctx_profile's classes), out[4i+1] / out[4i+2] = start / end in ms,
+   out[4i+3] = the launch's algorithmic work */
 int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records);
 /* microbenchmark of the planar-complex DMMA GEMM (instrumentation) */
 int fl_debug_zgemm(fl_ctx* ctx, int M, int N, int K, int batch, int iters, double* ms_out,

@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfeastlab_b200.so")
+# FEASTLAB_LIB: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("FEASTLAB_LIB") or os.path.join(HERE, "lib", "libfeastlab_b200.so")
 
 FL_OK, FL_INVALID_ARGUMENT, FL_RUNTIME_ERROR, FL_CHOLESKY, FL_SINGULAR_NODE, FL_CUDA, FL_NCCL, \
     FL_OOM = range(8)
@@ -57,6 +58,7 @@ _SIGS = {
     "fl_debug_panel_profile": (_I, [_P, _I]),
     "fl_ctx_profile_dump": (_I, [_P, _P, _I]),
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
+    "fl_zgemm_mode": (_I, [_I]),
     "fl_ctx_profile": (_I, [_P, C.c_char_p, _P, _P, _P, _P]),
     "fl_matrix_create": (_I, [_P, _P, _I, _I, _I, _PP, _P]),
     "fl_matrix_destroy": (_I, [_P]),

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -123,6 +124,8 @@ struct Profiler {
 
 }  // namespace
 
+struct fl_filter;
+
 struct fl_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -133,6 +136,9 @@ struct fl_ctx {
     Profiler prof;
     std::vector<cudaStream_t> aux;  // node-chunk streams (fork/join on `stream`)
     cudaEvent_t fork = nullptr;
+    cudaEvent_t done = nullptr;  // host waits: polled (see sync())
+    // filters whose singular-node flag is in flight (resolved by sync())
+    std::vector<fl_filter*> pending;
     std::vector<cudaEvent_t> join;
     std::vector<cudaStream_t> paux;  // per chunk: look-ahead panel stream (high priority)
     std::vector<cudaEvent_t> ev_panel, ev_next;
@@ -175,6 +181,28 @@ struct fl_filter {
     long w_stride = 0;
     int w_P = 0;
     DBuf y_tmp;
+    // CUDA graph of one whole application (non-cache mode): captured on the
+    // second call with an unchanged launch key, replayed while it holds
+    struct GraphKey {
+        const void *X, *Y, *fac, *w;
+        long ldx, ldy;
+        int p, slots, ns, zmode;
+        bool operator==(const GraphKey& o) const {
+            return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
+                   ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns && zmode == o.zmode;
+        }
+    };
+    GraphKey gkey{}, gseen{};
+    cudaGraphExec_t gexec = nullptr;
+    long long glaunches = 0;
+    // first singular node of the last application (0x7f7f7f7f: none), copied
+    // to pinned memory asynchronously and checked at the next host wait
+    int* h_bad = nullptr;
+    bool check_pending = false;
+    ~fl_filter() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (h_bad) cudaFreeHost(h_bad);
+    }
 };
 
 namespace {
@@ -229,7 +257,25 @@ void copy_out(fl_ctx* ctx, double* dst, long ldd, int n, const double* src, long
                          ctx->stream));
 }
 
-void sync(fl_ctx* ctx) { CK(cudaStreamSynchronize(ctx->stream)); }
+// Host wait for the context stream. Polls an event instead of a blocking
+// cudaStreamSynchronize: a blocked host thread woke up to ~100 ms late on
+// the GPU boxes, stalling the launch-paced pipeline behind it (measured:
+// 150 ms filter applications stretched to 250 ms at random).
+void resolve_pending(fl_ctx* ctx);
+
+void sync(fl_ctx* ctx) {
+    static const bool block = std::getenv("FEASTLAB_BLOCKING_SYNC") != nullptr;
+    if (block || !ctx->done) {
+        CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+        CK(cudaEventRecord(ctx->done, ctx->stream));
+        cudaError_t e;
+        while ((e = cudaEventQuery(ctx->done)) == cudaErrorNotReady) {
+        }
+        CK(e);
+    }
+    if (!ctx->pending.empty()) resolve_pending(ctx);
+}
 
 // --------------------------------------------------------------- profiling scope
 struct Prof {
@@ -356,7 +402,7 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
-    launch_check_diag(F, n, G, g0, f->bad.i(), st);
+    launch_check_diag(F, n, G, f->kb + g0, f->bad.i(), st);  // global node index
     launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, st);
 }
 
@@ -415,6 +461,15 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
     }
 }
 
+// FEASTLAB_GRAPHS=0 disables the CUDA-graph replay of filter applications
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FEASTLAB_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 size_t free_bytes() {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -460,68 +515,122 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         std::fill(f->factored.begin(), f->factored.end(), 0);
     }
     f->bad.ensure(sizeof(int) * 4);
-    int big = 0x7fffffff;
-    CK(cudaMemcpyAsync(f->bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    if (!f->h_bad) CK(cudaMallocHost(&f->h_bad, sizeof(int) * 4));
     // Node chunks run concurrently on the context's auxiliary streams so one
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
     const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
-    CK(cudaEventRecord(ctx->fork, ctx->stream));
-    for (int j = 0; j < ns; ++j) CK(cudaStreamWaitEvent(ctx->aux[j], ctx->fork, 0));
     long long new_facts = 0;
-    if (f->cache) {
-        // chunk j = nodes [j*L/ns, (j+1)*L/ns); factor the uncached ones, then solve
+    // everything below is stream work only (no host synchronisation), so a
+    // non-cache application is one CUDA graph: ~2.8k launches on 9 streams
+    // replayed with one cudaGraphLaunch instead of host-paced launches
+    auto enqueue = [&] {
+        CK(cudaMemsetAsync(f->bad.p, 0x7f, sizeof(int), ctx->stream));  // sentinel 0x7f7f7f7f
+        CK(cudaEventRecord(ctx->fork, ctx->stream));
+        for (int j = 0; j < ns; ++j) CK(cudaStreamWaitEvent(ctx->aux[j], ctx->fork, 0));
+        if (f->cache) {
+            // chunk j = nodes [j*L/ns, (j+1)*L/ns); factor the uncached ones, then solve
+            for (int j = 0; j < ns; ++j) {
+                const int c0 = (int)((long)L * j / ns), c1 = (int)((long)L * (j + 1) / ns);
+                int g = c0;
+                while (g < c1) {
+                    if (f->factored[g]) { ++g; continue; }
+                    int e = g;
+                    while (e < c1 && !f->factored[e]) ++e;
+                    factor_group(f, g, e - g, g, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
+                                 ctx->ev_next[j]);
+                    for (int k = g; k < e; ++k) f->factored[k] = 1;
+                    new_facts += e - g;
+                    g = e;
+                }
+                if (c1 > c0) solve_group(f, c0, c1 - c0, c0, X, ldx, P, ctx->aux[j]);
+            }
+        } else {
+            // rounds of `slots` nodes; round chunk j reuses slots [j*slots/ns, ...) on stream j
+            for (int g = 0; g < L; g += slots) {
+                const int G = std::min(slots, L - g);
+                const int nsr = std::min(ns, G);
+                for (int j = 0; j < nsr; ++j) {
+                    const int c0 = (int)((long)G * j / nsr), c1 = (int)((long)G * (j + 1) / nsr);
+                    const int s0 = (int)((long)slots * j / ns);
+                    factor_group(f, g + c0, c1 - c0, s0, ctx->aux[j], ctx->paux[j],
+                                 ctx->ev_panel[j], ctx->ev_next[j]);
+                    solve_group(f, g + c0, c1 - c0, s0, X, ldx, P, ctx->aux[j]);
+                }
+            }
+            new_facts = f->nc;
+        }
         for (int j = 0; j < ns; ++j) {
-            const int c0 = (int)((long)L * j / ns), c1 = (int)((long)L * (j + 1) / ns);
-            int g = c0;
-            while (g < c1) {
-                if (f->factored[g]) { ++g; continue; }
-                int e = g;
-                while (e < c1 && !f->factored[e]) ++e;
-                factor_group(f, g, e - g, g, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
-                             ctx->ev_next[j]);
-                for (int k = g; k < e; ++k) f->factored[k] = 1;
-                new_facts += e - g;
-                g = e;
-            }
-            if (c1 > c0) solve_group(f, c0, c1 - c0, c0, X, ldx, P, ctx->aux[j]);
+            CK(cudaEventRecord(ctx->join[j], ctx->aux[j]));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->join[j], 0));
         }
-    } else {
-        // rounds of `slots` nodes; round chunk j reuses slots [j*slots/ns, ...) on stream j
-        for (int g = 0; g < L; g += slots) {
-            const int G = std::min(slots, L - g);
-            const int nsr = std::min(ns, G);
-            for (int j = 0; j < nsr; ++j) {
-                const int c0 = (int)((long)G * j / nsr), c1 = (int)((long)G * (j + 1) / nsr);
-                const int s0 = (int)((long)slots * j / ns);
-                factor_group(f, g + c0, c1 - c0, s0, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
-                             ctx->ev_next[j]);
-                solve_group(f, g + c0, c1 - c0, s0, X, ldx, P, ctx->aux[j]);
-            }
+        // ordered accumulation over the local nodes
+        NodeShifts w{};
+        for (int b = 0; b < L; ++b) {
+            w.zr[b] = f->wr[f->kb + b];
+            w.zi[b] = f->wi[f->kb + b];
         }
+        ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
+        if (L > 0) {
+            Prof pr(ctx, P_ACCUM, (16.0 * L + 8.0) * N * P);
+            launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
+        } else {
+            CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
+        }
+        if (ctx->comm) {
+            if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
+            Prof pr(ctx, P_ALLREDUCE, 8.0 * N * p, 0);
+            nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm,
+                                     ctx->stream),
+                       "ncclAllReduce(Y)");
+            // every rank learns the first singular node, so all of them throw
+            nccl_check(ncclAllReduce(f->bad.p, f->bad.p, 1, ncclInt32, ncclMin, ctx->comm,
+                                     ctx->stream),
+                       "ncclAllReduce(bad node)");
+        }
+    };
+    const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
+                                  zgemm_mode()};
+    const bool graphable = !f->cache && !ctx->prof.on && graphs_enabled();
+    if (graphable && f->gexec && f->gkey == key) {
+        CK(cudaGraphLaunch(f->gexec, ctx->stream));
+        g_launch_count += f->glaunches;
         new_facts = f->nc;
-    }
-    for (int j = 0; j < ns; ++j) {
-        CK(cudaEventRecord(ctx->join[j], ctx->aux[j]));
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->join[j], 0));
-    }
-    {
-        int h_bad = 0;
-        CK(cudaMemcpyAsync(&h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
-        if (h_bad != 0x7fffffff) {
-            const int k = f->kb + h_bad;
-            if (f->cache) std::fill(f->factored.begin(), f->factored.end(), 0);
-            else if (facts) *facts += h_bad;  // nodes factored before it (filterop.cpp:74-76)
-            char buf[256];
-            std::snprintf(buf, sizeof(buf),
-                          "factorize_node: singular factorization at node %d (z = %f+%fi)", k,
-                          f->zr[k], f->zi[k]);
-            Fail fl{FL_SINGULAR_NODE, buf};
-            fl.index = k;
-            fl.zr = f->zr[k];
-            fl.zi = f->zi[k];
-            throw fl;
+    } else if (graphable && f->gseen == key) {
+        if (f->gexec) {
+            cudaGraphExecDestroy(f->gexec);
+            f->gexec = nullptr;
         }
+        const long long l0 = g_launch_count;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+        cudaGraph_t graph = nullptr;
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(ctx->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CK(cudaStreamEndCapture(ctx->stream, &graph));
+        // keep the look-ahead panel stream's priority on its captured kernel nodes
+        const cudaError_t e =
+            cudaGraphInstantiate(&f->gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
+        cudaGraphDestroy(graph);
+        CK(e);
+        f->glaunches = g_launch_count - l0;
+        f->gkey = key;
+        CK(cudaGraphLaunch(f->gexec, ctx->stream));
+    } else {
+        f->gseen = key;
+        enqueue();
+    }
+    // the singular-node verdict travels to pinned memory behind the work; the
+    // host does not wait for it here (a host round trip per application
+    // exposed host scheduling jitter to the GPU timeline): the next sync() on
+    // the context -- every host-returning call makes one -- raises it
+    CK(cudaMemcpyAsync(f->h_bad, f->bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (!f->check_pending) {
+        f->check_pending = true;
+        ctx->pending.push_back(f);
     }
     if (f->cache && ctx->comm) {
         // factorizations are counted globally: every rank adds the same total
@@ -535,27 +644,30 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         sync(ctx);
         new_facts = tot;
     }
-    // ordered accumulation over the local nodes
-    NodeShifts w{};
-    for (int b = 0; b < L; ++b) {
-        w.zr[b] = f->wr[f->kb + b];
-        w.zi[b] = f->wi[f->kb + b];
-    }
-    ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
-    if (L > 0) {
-        Prof pr(ctx, P_ACCUM, (16.0 * L + 8.0) * N * P);
-        launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
-    } else {
-        CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
-    }
-    if (ctx->comm) {
-        if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
-        Prof pr(ctx, P_ALLREDUCE, 8.0 * N * p, 0);
-        nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm, ctx->stream),
-                   "ncclAllReduce(Y)");
-    }
     if (rhs) *rhs += (long long)f->nc * p;
     if (facts) *facts += new_facts;
+}
+
+// Raise the first singular node among the applications whose verdicts have
+// arrived (called by sync() after the stream drained).
+void resolve_pending(fl_ctx* ctx) {
+    fl_filter* bad = nullptr;
+    for (fl_filter* f : ctx->pending) {
+        f->check_pending = false;
+        if (!bad && *f->h_bad != 0x7f7f7f7f) bad = f;
+    }
+    ctx->pending.clear();
+    if (!bad) return;
+    const int k = *bad->h_bad;
+    if (bad->cache) std::fill(bad->factored.begin(), bad->factored.end(), 0);
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "factorize_node: singular factorization at node %d (z = %f+%fi)",
+                  k, bad->zr[k], bad->zi[k]);
+    Fail fl{FL_SINGULAR_NODE, buf};
+    fl.index = k;
+    fl.zr = bad->zr[k];
+    fl.zi = bad->zi[k];
+    throw fl;
 }
 
 // --------------------------------------------------------------- Rayleigh-Ritz helpers
@@ -828,12 +940,15 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         for (int j = 0; j < naux; ++j) {
             CK(cudaStreamCreateWithFlags(&c->aux[j], cudaStreamNonBlocking));
             // panels are the critical path: highest priority
-            CK(cudaStreamCreateWithPriority(&c->paux[j], cudaStreamNonBlocking, prio_hi));
+            const char* pe = std::getenv("FEASTLAB_PANEL_PRIO");
+            CK(cudaStreamCreateWithPriority(&c->paux[j], cudaStreamNonBlocking,
+                                            (pe && pe[0] == '0') ? prio_lo : prio_hi));
             CK(cudaEventCreateWithFlags(&c->join[j], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_panel[j], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_next[j], cudaEventDisableTiming));
         }
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
         c->rank = rank;
         c->nranks = nranks;
         if (id != nullptr) {  // a clique (also of one rank: exercises the NCCL path)
@@ -882,6 +997,7 @@ int fl_ctx_destroy(fl_ctx* ctx) {
     for (cudaEvent_t e : ctx->ev_panel) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->ev_next) cudaEventDestroy(e);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->done) cudaEventDestroy(ctx->done);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return FL_OK;
@@ -904,8 +1020,8 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
 
-// timeline of the profiled launches: out[3*i] = class, [3*i+1] = start ms,
-// [3*i+2] = end ms (relative to the first recorded event); returns the count
+// timeline of the profiled launches: out[4*i] = class, [4*i+1] = start ms,
+// [4*i+2] = end ms (relative to the first recorded event), [4*i+3] = work; returns the count
 int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
     CtxLock lk(ctx);
     cudaStreamSynchronize(ctx->stream);
@@ -919,9 +1035,10 @@ int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
         float a = 0.f, b = 0.f;
         cudaEventElapsedTime(&a, base, r.a);
         cudaEventElapsedTime(&b, base, r.b);
-        out[3 * n] = r.cls;
-        out[3 * n + 1] = a;
-        out[3 * n + 2] = b;
+        out[4 * n] = r.cls;
+        out[4 * n + 1] = a;
+        out[4 * n + 2] = b;
+        out[4 * n + 3] = r.work;
         ++n;
     }
     return n;
@@ -957,6 +1074,11 @@ int fl_debug_zgemm(fl_ctx* ctx, int M, int Nc, int K, int batch, int iters, doub
         cudaEventDestroy(e1);
         *ms_out = ms / iters;
     });
+}
+
+int fl_zgemm_mode(int mode) {
+    if (mode >= 0) set_zgemm_mode(mode);
+    return zgemm_mode();
 }
 
 int fl_debug_panel_profile(double* out8, int reset) {
@@ -1147,7 +1269,10 @@ int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr,
 
 int fl_filter_destroy(fl_filter* f) {
     if (f) {
-        cudaSetDevice(f->ctx->device);
+        CtxLock lk(f->ctx);
+        cudaStreamSynchronize(f->ctx->stream);  // in-flight verdict copy into f->h_bad
+        auto& pend = f->ctx->pending;
+        pend.erase(std::remove(pend.begin(), pend.end(), f), pend.end());
         delete f;
     }
     return FL_OK;
@@ -1184,9 +1309,23 @@ int fl_filter_apply_raw(fl_filter* f, const double* X, int ldx, int p, double* Y
         double* Ys = Xs + (size_t)N * P;
         CK(cudaMemsetAsync(Xs, 0, sizeof(double) * (size_t)N * P, ctx->stream));
         copy_in(ctx, Xs, N, n, X, ldx, p, loc);
-        filter_apply_dev(f, Xs, N, p, Ys, N, rhs, facts);
+        if (loc == FL_DEVICE) {  // stays asynchronous: a singular node is raised by the next sync
+            filter_apply_dev(f, Xs, N, p, Ys, N, rhs, facts);
+            copy_out(ctx, Y, ldy, n, Ys, N, p, loc);
+            return;
+        }
+        long long r = 0, fa = 0;
+        filter_apply_dev(f, Xs, N, p, Ys, N, &r, &fa);
         copy_out(ctx, Y, ldy, n, Ys, N, p, loc);
-        if (loc == FL_HOST) sync(ctx);
+        try {
+            sync(ctx);
+        } catch (const Fail& e) {
+            // nodes factored before the singular one count (filterop.cpp:74-76)
+            if (e.code == FL_SINGULAR_NODE && !f->cache && facts) *facts += e.index;
+            throw;
+        }
+        if (rhs) *rhs += r;
+        if (facts) *facts += fa;
     });
 }
 

@@ -5,7 +5,10 @@
 // a cp.async multi-stage ring; fragments are read from padded shared memory
 // with conflict-free 8-byte loads:
 //   "MK" operand layout (64-dim contiguous in global):  smem[k][x], ld 68
-//   "KM" operand layout (k contiguous in global):        smem[x][k], ld 20
+//   "KM" operand layout (k contiguous in global):        smem[x][k ^ 4(x&3)], ld 16
+// (the XOR swizzle spreads a fragment read's 8 rows x 4 k over all 16
+// 8-byte bank pairs without padding, so a 2-stage planar-complex ring is
+// 66 KB and three CTAs fit on one SM).
 // Complex operands are planar (separate Re / Im planes), so each DMMA tile is
 // purely real; a complex multiply-add is 4 real DMMAs (no 3M trick: keeps the
 // rounding of the 4M product the reference's std::complex arithmetic has).
@@ -17,29 +20,33 @@ namespace fl {
 constexpr int GB = 64;       // CTA tile (M and N)
 constexpr int GK = 16;       // k depth per stage
 constexpr int LD_MK = GB + 4;  // 68
-constexpr int LD_KM = GK + 4;  // 20
-constexpr int TILE_DOUBLES = (GK * LD_MK > GB * LD_KM) ? GK * LD_MK : GB * LD_KM;  // 1280
+constexpr int LD_KM = GK;      // 16, swizzled
+constexpr int MK_DOUBLES = GK * LD_MK;  // 1088
+constexpr int KM_DOUBLES = GB * LD_KM;  // 1024
+constexpr int TILE_DOUBLES = MK_DOUBLES;  // >= either layout
+
+FL_DEV int km_index(int x, int k) { return x * LD_KM + (k ^ ((x & 3) << 2)); }
 
 // Copy one 64x16 operand tile (one plane) into shared memory.
 //  KC=false: global column-major with the 64-dim contiguous: tile columns are k.
 //  KC=true : global column-major with k contiguous: tile columns are the 64-dim.
-template <bool KC>
+template <bool KC, int NT = 128>
 FL_DEV void load_tile(double* sm, const double* g, long ld, int tid) {
     if (!KC) {
         // 16 columns x 64 doubles = 16 x 32 chunks of 16 B
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int c = tid + i * 128;
+        for (int i = 0; i < 512 / NT; ++i) {
+            int c = tid + i * NT;
             int col = c >> 5, ch = c & 31;
             cp_async16(sm + col * LD_MK + ch * 2, g + col * ld + ch * 2);
         }
     } else {
         // 64 columns x 16 doubles = 64 x 8 chunks
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int c = tid + i * 128;
+        for (int i = 0; i < 512 / NT; ++i) {
+            int c = tid + i * NT;
             int col = c >> 3, ch = c & 7;
-            cp_async16(sm + col * LD_KM + ch * 2, g + col * ld + ch * 2);
+            cp_async16(sm + km_index(col, ch * 2), g + col * ld + ch * 2);
         }
     }
 }
@@ -47,7 +54,7 @@ FL_DEV void load_tile(double* sm, const double* g, long ld, int tid) {
 // Fragment element (x, k) of a tile in shared memory.
 template <bool KC>
 FL_DEV double frag(const double* sm, int x, int k) {
-    return KC ? sm[x * LD_KM + k] : sm[k * LD_MK + x];
+    return KC ? sm[km_index(x, k)] : sm[k * LD_MK + x];
 }
 
 // Offset of global tile (x0, k0) for an operand of the given layout.

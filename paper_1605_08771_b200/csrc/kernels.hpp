@@ -26,6 +26,9 @@ struct ZGemm {
     double *Cr, *Ci; long ldc; long strideC;
 };
 void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s);
+// Complex product form of the zgemm launches: 1 = 3M (default), 0 = 4M.
+int zgemm_mode();
+void set_zgemm_mode(int mode);
 // Planar complex C = A B (in place with B == C allowed: each CTA reads its
 // whole K range before storing).
 void launch_zgemm_set(const ZGemm& g, int batch, cudaStream_t s);

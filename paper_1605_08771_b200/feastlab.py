@@ -155,6 +155,16 @@ def set_default_context(ctx: Context | None) -> None:
     _tls.ctx = ctx
 
 
+def zgemm_mode(mode: str | None = None) -> str:
+    """Complex product form of the filter's DMMA GEMMs, process-wide: "3m"
+    (three real products per complex product; default) or "4m". With no
+    argument only reports the mode in effect."""
+    if mode not in (None, "3m", "4m"):
+        raise ValueError("zgemm_mode: mode must be '3m' or '4m'")
+    code = -1 if mode is None else (1 if mode == "3m" else 0)
+    return "3m" if L.lib().fl_zgemm_mode(code) == 1 else "4m"
+
+
 def device_count() -> int:
     c = C.c_int()
     L.lib().fl_device_count(C.byref(c))

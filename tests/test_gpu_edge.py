@@ -71,3 +71,22 @@ def test_run_to_run_bitwise_determinism():
         assert P.write_trace_csv(a.trace) == P.write_trace_csv(b.trace)
         assert np.array_equal(a.eigenvalues, b.eigenvalues)
         assert np.array_equal(a.eigenvectors, b.eigenvectors)
+
+
+def test_singular_node_device_path_is_raised_at_next_sync():
+    """Device-resident applications do not wait for the singular-node verdict;
+    the next host wait on the context raises it (capi.cu resolve_pending)."""
+    import torch
+    import paper_1605_08771_b200 as P
+    ctx = P.Context(0)
+    A = np.eye(70)
+    A[3, 3] = np.inf
+    f = P.FilterApplier(A, P.build_contour_rule(P.SearchInterval(-1, 1), 4), ctx=ctx)
+    X = torch.ones((2, 70), dtype=torch.float64, device="cuda")
+    Y = torch.empty_like(X)
+    torch.cuda.synchronize()
+    f.apply_device(X.data_ptr(), 70, 2, Y.data_ptr(), 70)  # returns without waiting
+    with pytest.raises(P.FeastRuntimeError) as ei:
+        ctx.sync()
+    assert "singular factorization at node 0" in str(ei.value)
+    ctx.sync()  # the verdict is consumed once

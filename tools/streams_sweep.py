@@ -10,7 +10,7 @@ X = np.asfortranarray(np.random.default_rng(1).standard_normal((n, p)))
 rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.2), nc)
 f = P.FilterApplier(A, rule, ctx=ctx)
 F = nc * (8 / 3 * n ** 3 + 8 * n * n * p)
-for s in (1, 2, 4):
+for s in [int(a) for a in sys.argv[4:]] or (1, 2, 3, 4):
     ctx.set_streams(s)
     f.apply(X)
     t0 = time.time()

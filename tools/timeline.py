@@ -14,10 +14,10 @@ ctx.set_streams(streams)
 f.apply(X)
 ctx.set_profiling(True)
 f.apply(X)
-buf = (ctypes.c_double * (3 * 200000))()
+buf = (ctypes.c_double * (4 * 200000))()
 cnt = _lib.lib().fl_ctx_profile_dump(ctx.handle, buf, 200000)
 ctx.set_profiling(False)
-rec = np.frombuffer(buf, dtype=np.float64, count=3 * cnt).reshape(-1, 3)
+rec = np.frombuffer(buf, dtype=np.float64, count=4 * cnt).reshape(-1, 4)
 names = ["shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate", "allreduce"]
 T = rec[:, 2].max()
 print(f"n={n} p={p} nc={nc} streams={streams}: span {T:.1f} ms, {cnt} records")
@@ -28,7 +28,7 @@ for ci, nm in enumerate(names):
     r = rec[rec[:, 0] == ci]
     if len(r) == 0: continue
     act = np.zeros(len(grid), bool)
-    for a, b in r[:, 1:]:
+    for a, b in r[:, 1:3]:
         act[(grid >= a) & (grid < b)] = True
     busy[nm] = act
     print(f"  {nm:10s} busy {100*act.mean():5.1f}% of span ({act.mean()*T:.1f} ms)")
@@ -42,3 +42,15 @@ if "panel" in busy and "zgemm" in busy:
 perm = rec[rec[:, 0] == 5]
 if len(perm):
     print(f"  first solve starts at {perm[:,1].min():.1f} ms, last at {perm[:,1].max():.1f} ms")
+# zgemm launches by work size: efficiency per bucket (launch-duration based)
+z = rec[rec[:, 0] == 4]
+if len(z):
+    dur = z[:, 2] - z[:, 1]
+    w = z[:, 3]
+    print(f"  zgemm: {len(z)} launches, {w.sum()/dur.sum()/1e9:.2f} TF/s avg over launch durations")
+    edges = [0, 1e9, 1e10, 5e10, 1e11, 2e11, 1e13]
+    for lo, hi in zip(edges[:-1], edges[1:]):
+        m = (w >= lo) & (w < hi)
+        if m.any():
+            print(f"    work [{lo:.0e},{hi:.0e}): {m.sum():4d} launches, {dur[m].sum():7.2f} ms, "
+                  f"{w[m].sum()/dur[m].sum()/1e9:6.2f} TF/s")
