@@ -13,11 +13,15 @@ namespace feastlab {
 class SymmetricMatrix {
 public:
     explicit SymmetricMatrix(MatrixXd entries, double sym_tol = 1e-12);
+    /// Same, reading a column-major n x n matrix (leading dimension lda) in
+    /// place: no intermediate copy of the caller's buffer.
+    SymmetricMatrix(const double* entries, int n, long lda, double sym_tol = 1e-12);
     int dim() const { return mat_.rows(); }
     const MatrixXd& mat() const { return mat_; }
     double operator()(int i, int j) const { return mat_(i, j); }
 
 private:
+    void init(const double* entries, int n, long lda, double sym_tol);
     MatrixXd mat_;
 };
 

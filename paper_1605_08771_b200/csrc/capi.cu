@@ -132,11 +132,16 @@ struct fl_ctx {
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
     std::recursive_mutex mu;
+    // the owner's reference plus one per live matrix / block / filter: a
+    // context outlives its objects whatever order callers (or a garbage
+    // collector breaking a reference cycle) destroy them in
+    std::atomic<int> refs{1};
     long long launches_at_create = 0;
     Profiler prof;
     std::vector<cudaStream_t> aux;  // node-chunk streams (fork/join on `stream`)
     cudaEvent_t fork = nullptr;
     cudaEvent_t done = nullptr;  // host waits: polled (see sync())
+    unsigned long long* h_cnt = nullptr;  // pinned: eigensolver sweep counter
     // filters whose singular-node flag is in flight (resolved by sync())
     std::vector<fl_filter*> pending;
     std::vector<cudaEvent_t> join;
@@ -685,6 +690,21 @@ void device_sym_eig(fl_ctx* ctx, double* M, long ldm, int p, int P, double* vals
     double fro2 = 0.0;
     CK(cudaMemcpyAsync(&fro2, ctx->scal.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     sync(ctx);
+    static const bool scalar = [] {
+        const char* e = std::getenv("FEASTLAB_EIG");
+        return e && std::strcmp(e, "scalar") == 0;
+    }();
+    if (!scalar) {
+        // block Jacobi (ritz.cu); the output V doubles as its Q-block buffer
+        int sweeps = 0;
+        const int rc = block_jacobi_eig(M, ldm, p, P, std::sqrt(fro2), work, Vtmp, V, vals, V, P,
+                                        reinterpret_cast<unsigned long long*>(ctx->cnt.p),
+                                        ctx->h_cnt, 40, &sweeps, ctx->stream);
+        g_launch_count += 2 + 2LL * sweeps * (P / 32 - 1);
+        if (rc != 0) throw Fail{FL_CUDA, "block_jacobi_eig failed"};
+        CK(cudaGetLastError());
+        return;
+    }
     CK(cudaMemsetAsync(V, 0, sizeof(double) * (size_t)P * P, ctx->stream));
     CK(cudaMemsetAsync(Vtmp, 0, sizeof(double) * (size_t)P * P, ctx->stream));
     const int rc = jacobi_eig(M, ldm, p, std::sqrt(fro2), work, Vtmp, P, vals, V, P,
@@ -949,6 +969,7 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         }
         CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+        CK(cudaMallocHost(&c->h_cnt, sizeof(unsigned long long)));
         c->rank = rank;
         c->nranks = nranks;
         if (id != nullptr) {  // a clique (also of one rank: exercises the NCCL path)
@@ -980,8 +1001,7 @@ int fl_nccl_unique_id(void* out128, fl_err* err) {
     });
 }
 
-int fl_ctx_destroy(fl_ctx* ctx) {
-    if (!ctx) return FL_OK;
+static void ctx_teardown(fl_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -998,8 +1018,19 @@ int fl_ctx_destroy(fl_ctx* ctx) {
     for (cudaEvent_t e : ctx->ev_next) cudaEventDestroy(e);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->done) cudaEventDestroy(ctx->done);
+    if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
+}
+
+static void ctx_retain(fl_ctx* ctx) { ctx->refs.fetch_add(1); }
+
+static void ctx_release(fl_ctx* ctx) {
+    if (ctx->refs.fetch_sub(1) == 1) ctx_teardown(ctx);
+}
+
+int fl_ctx_destroy(fl_ctx* ctx) {
+    if (ctx) ctx_release(ctx);
     return FL_OK;
 }
 
@@ -1137,14 +1168,19 @@ int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_m
         CK(cudaMemsetAsync(m->buf.p, 0, sizeof(double) * (size_t)m->N * m->N, ctx->stream));
         copy_in(ctx, m->d(), m->N, n, A, lda, n, loc);
         sync(ctx);
+        ctx_retain(ctx);
         *out = m.release();
     });
 }
 
 int fl_matrix_destroy(fl_matrix* m) {
     if (m) {
-        cudaSetDevice(m->ctx->device);
-        delete m;
+        fl_ctx* ctx = m->ctx;
+        {
+            CtxLock lk(ctx);
+            delete m;
+        }
+        ctx_release(ctx);
     }
     return FL_OK;
 }
@@ -1160,14 +1196,19 @@ int fl_block_create(fl_ctx* ctx, int n, int cap_cols, fl_block** out, fl_err* er
         b->n = n;
         b->N = round_up(n, FL_TILE);
         block_reserve(b.get(), std::max(cap_cols, 1));
+        ctx_retain(ctx);
         *out = b.release();
     });
 }
 
 int fl_block_destroy(fl_block* b) {
     if (b) {
-        cudaSetDevice(b->ctx->device);
-        delete b;
+        fl_ctx* ctx = b->ctx;
+        {
+            CtxLock lk(ctx);
+            delete b;
+        }
+        ctx_release(ctx);
     }
     return FL_OK;
 }
@@ -1263,17 +1304,22 @@ int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr,
         // contiguous node shard of this rank
         fl_node_shard(n_c, ctx->rank, ctx->nranks, &f->kb, &f->ke);
         f->factored.assign(f->ke - f->kb, 0);
+        ctx_retain(ctx);
         *out = f.release();
     });
 }
 
 int fl_filter_destroy(fl_filter* f) {
     if (f) {
-        CtxLock lk(f->ctx);
-        cudaStreamSynchronize(f->ctx->stream);  // in-flight verdict copy into f->h_bad
-        auto& pend = f->ctx->pending;
-        pend.erase(std::remove(pend.begin(), pend.end(), f), pend.end());
-        delete f;
+        fl_ctx* ctx = f->ctx;
+        {
+            CtxLock lk(ctx);
+            cudaStreamSynchronize(ctx->stream);  // in-flight verdict copy into f->h_bad
+            auto& pend = ctx->pending;
+            pend.erase(std::remove(pend.begin(), pend.end(), f), pend.end());
+            delete f;
+        }
+        ctx_release(ctx);
     }
     return FL_OK;
 }

@@ -64,9 +64,7 @@ int fl_solve(fl_ctx* ctx, int variant, const double* A, int n, int lda, double l
     return guarded(err, [&] {
         if (n < 1 || lda < n) throw std::invalid_argument("fl_solve: bad matrix shape");
         ScopedContext sc(ctx);
-        MatrixXd M(n, n);
-        for (int j = 0; j < n; ++j) std::memcpy(M.col(j), A + (size_t)j * lda, sizeof(double) * n);
-        const SymmetricMatrix S(std::move(M));
+        const SymmetricMatrix S(A, n, lda);
         SolverConfig cfg;
         cfg.m0 = c->m0;
         cfg.n_c = c->n_c;
@@ -142,9 +140,7 @@ int fl_symmetric_matrix(const double* M, int n, int ldm, double sym_tol, double*
     return guarded(err, [&] {
         if (n < 1 || ldm < n)
             throw std::invalid_argument("SymmetricMatrix: matrix must be square, n >= 1");
-        MatrixXd E(n, n);
-        for (int j = 0; j < n; ++j) std::memcpy(E.col(j), M + (size_t)j * ldm, sizeof(double) * n);
-        SymmetricMatrix S(std::move(E), sym_tol);
+        SymmetricMatrix S(M, n, ldm, sym_tol);
         std::memcpy(out, S.mat().data(), sizeof(double) * (size_t)n * n);
     });
 }

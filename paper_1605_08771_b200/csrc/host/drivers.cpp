@@ -41,7 +41,7 @@ struct PhaseTimer {
     bool on = std::getenv("FEASTLAB_TIME") != nullptr;
     fl_ctx* ctx;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-    double filter = 0, orth = 0, rr = 0, host = 0;
+    double filter = 0, orth = 0, rr = 0, host = 0, setup = 0, upload = 0, guess = 0;
     explicit PhaseTimer(fl_ctx* c) : ctx(c) {}
     void lap(double& acc) {
         if (!on) return;
@@ -53,8 +53,9 @@ struct PhaseTimer {
     }
     ~PhaseTimer() {
         if (on)
-            std::fprintf(stderr, "feast_solve phases [s]: filter %.3f orthonormalize %.3f "
-                                 "rayleigh_ritz %.3f host %.3f\n", filter, orth, rr, host);
+            std::fprintf(stderr, "feast_solve phases [s]: matrix upload %.3f initial guess %.3f "
+                                 "setup %.3f filter %.3f orthonormalize %.3f rayleigh_ritz %.3f "
+                                 "host %.3f\n", upload, guess, setup, filter, orth, rr, host);
     }
 };
 
@@ -185,16 +186,19 @@ MatrixXd make_initial_guess(int n, int m0, std::uint64_t seed) {
 Solution feast_solve(const SymmetricMatrix& A, const SearchInterval& interval,
                      const SolverConfig& config) {
     validate_config(A, config);
+    fl_ctx* ctx = current_context();
+    PhaseTimer timer(ctx);
     const ContourRule rule = build_contour_rule(interval, config.n_c);
     FilterApplier filt(A, rule, config.cache_factorizations);
-    fl_ctx* ctx = current_context();
+    timer.lap(timer.upload);
     const int n = A.dim();
     Solution sol;
     DeviceBlock X = initial_block(ctx, A, config);
+    timer.lap(timer.guess);
     DeviceBlock Y(ctx, n, config.m0), U(ctx, n, config.m0);
     DevRitz rr(ctx, n);
     int last_m_found = 0;
-    PhaseTimer timer(ctx);
+    timer.lap(timer.setup);
     for (int iter = 1; iter <= config.max_iter; ++iter) {
         timer.lap(timer.host);
         filt.apply(X, Y, sol.accounting);

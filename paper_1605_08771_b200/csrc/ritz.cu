@@ -590,6 +590,272 @@ int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, 
     return 0;
 }
 
+// ------------------------------------------------------------------ block Jacobi
+// Two-sided block Jacobi (cyclic round-robin over 32-wide column blocks):
+// per outer round, each of the P/64 disjoint block pairs (a, b) is solved in
+// one CTA by cyclic scalar Jacobi in shared memory (same sym.schur2
+// rotations and skip threshold eps ||A||_F as above), giving a 64 x 64
+// orthogonal Q_ab; then one launch applies all of them: A[I, J] <- Q_I^T
+// A[I, J] Q_J for every pair-tile (I, J) and V[:, J] <- V[:, J] Q_J. An outer
+// sweep visits every block pair once, so a sweep that rotates nothing leaves
+// every |a_pq| <= thr: the scalar kernel's stopping rule. Grid-wide
+// synchronisation drops from p - 1 barriers per sweep to 2 (P/32 - 1).
+constexpr int BJ = 32;       // column block
+constexpr int BJ2 = 2 * BJ;  // pair subproblem
+constexpr int BJL = BJ2 + 1; // padded smem leading dimension
+
+__device__ __forceinline__ int bj_global(int l, int ia, int ib) {
+    return l < BJ ? ia * BJ + l : ib * BJ + (l - BJ);
+}
+
+__global__ void __launch_bounds__(256) bj_inner_kernel(const double* __restrict__ W, long ld, int nb,
+                                                       int r, double thr, int max_inner,
+                                                       double* __restrict__ Qbuf,
+                                                       unsigned long long* cnt) {
+    extern __shared__ double bsm[];
+    double* S = bsm;              // [BJ2][BJL], column-major
+    double* Q = bsm + BJ2 * BJL;  // [BJ2][BJL]
+    __shared__ double rc[BJ], rs[BJ], rt[BJ];
+    __shared__ int pa[BJ], pb[BJ];
+    __shared__ int any;
+    const int tid = threadIdx.x;
+    int ia, ib;
+    round_pair(r, blockIdx.x, nb, ia, ib);
+    for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+        const int lr = e % BJ2, lc = e / BJ2;
+        S[lc * BJL + lr] = W[(long)bj_global(lc, ia, ib) * ld + bj_global(lr, ia, ib)];
+        Q[lc * BJL + lr] = (lr == lc) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    unsigned long long rot = 0;
+    for (int sw = 0; sw < max_inner; ++sw) {
+        if (tid == 0) any = 0;
+        __syncthreads();
+        for (int rr = 0; rr < BJ2 - 1; ++rr) {
+            if (tid < BJ) {
+                int a, b;
+                round_pair(rr, tid, BJ2, a, b);
+                const double apq = S[b * BJL + a], app = S[a * BJL + a], aqq = S[b * BJL + b];
+                double c = 1.0, sn_ = 0.0, t = 0.0;
+                if (fabs(apq) > thr) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    sn_ = t * c;
+                    ++rot;
+                    any = 1;
+                }
+                pa[tid] = a;
+                pb[tid] = b;
+                rc[tid] = c;
+                rs[tid] = sn_;
+                rt[tid] = t;
+            }
+            __syncthreads();
+            // S <- J^T S J on 2 x 2 blocks (P rows, Q cols), in place
+            for (int e = tid; e < BJ * BJ; e += blockDim.x) {
+                const int P = e % BJ, Qc = e / BJ;
+                const double s1 = rs[P], s2 = rs[Qc];
+                if (s1 == 0.0 && s2 == 0.0) continue;
+                const int a1 = pa[P], b1 = pb[P], a2 = pa[Qc], b2 = pb[Qc];
+                const double c1 = rc[P], c2 = rc[Qc];
+                const double Baa = S[a2 * BJL + a1], Bab = S[b2 * BJL + a1];
+                const double Bba = S[a2 * BJL + b1], Bbb = S[b2 * BJL + b1];
+                double naa, nab, nba, nbb;
+                if (P == Qc) {
+                    const double t = rt[P];
+                    naa = Baa - t * Bab;
+                    nbb = Bbb + t * Bab;
+                    nab = 0.0;
+                    nba = 0.0;
+                } else {
+                    const double ra_a = c1 * Baa - s1 * Bba, ra_b = c1 * Bab - s1 * Bbb;
+                    const double rb_a = s1 * Baa + c1 * Bba, rb_b = s1 * Bab + c1 * Bbb;
+                    naa = ra_a * c2 - ra_b * s2;
+                    nab = ra_a * s2 + ra_b * c2;
+                    nba = rb_a * c2 - rb_b * s2;
+                    nbb = rb_a * s2 + rb_b * c2;
+                }
+                S[a2 * BJL + a1] = naa;
+                S[b2 * BJL + a1] = nab;
+                S[a2 * BJL + b1] = nba;
+                S[b2 * BJL + b1] = nbb;
+            }
+            // Q <- Q J
+            for (int e = tid; e < BJ2 * BJ; e += blockDim.x) {
+                const int x = e % BJ2, P = e / BJ2;
+                const double sn_ = rs[P];
+                if (sn_ == 0.0) continue;
+                const double c = rc[P];
+                const double qa = Q[pa[P] * BJL + x], qb = Q[pb[P] * BJL + x];
+                Q[pa[P] * BJL + x] = c * qa - sn_ * qb;
+                Q[pb[P] * BJL + x] = sn_ * qa + c * qb;
+            }
+            __syncthreads();
+        }
+        if (!any) break;
+        __syncthreads();
+    }
+    double* Qo = Qbuf + (long)blockIdx.x * BJ2 * BJ2;
+    for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+        const int lr = e % BJ2, lc = e / BJ2;
+        Qo[lc * BJ2 + lr] = Q[lc * BJL + lr];
+    }
+    if (tid < BJ) {
+        for (int off = 16; off > 0; off >>= 1) rot += __shfl_xor_sync(0xffffffffu, rot, off);
+        if (tid == 0 && rot) atomicAdd(cnt, rot);
+    }
+}
+
+// C (64 x 64, smem ld BJL) = op(X) Y with X, Y 64 x 64 in smem (ld BJL);
+// TX: X transposed. 256 threads, 4 x 4 outputs each.
+template <bool TX>
+__device__ __forceinline__ void bj_mm(const double* X, const double* Y, double* C) {
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k = 0; k < BJ2; ++k) {
+        double xv[4], yv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int row = ty + 16 * i;
+            xv[i] = TX ? X[row * BJL + k] : X[k * BJL + row];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) yv[j] = Y[(tx + 16 * j) * BJL + k];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(xv[i], yv[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) C[(tx + 16 * j) * BJL + ty + 16 * i] = acc[i][j];
+}
+
+// CTA t < ntA: A pair-tile (I, J), I <= J (symmetric: the transposed tile is
+// written too); otherwise a 64-row tile of V times Q_J.
+__global__ void __launch_bounds__(256) bj_update_kernel(double* __restrict__ W, long ld,
+                                                        double* __restrict__ V, long ldv, int P,
+                                                        int nb, int r,
+                                                        const double* __restrict__ Qbuf) {
+    extern __shared__ double usm[];
+    double* X = usm;
+    double* QI = usm + BJ2 * BJL;
+    double* QJ = usm + 2 * BJ2 * BJL;
+    double* T = usm + 3 * BJ2 * BJL;
+    const int np = nb / 2;
+    const int ntA = np * (np + 1) / 2;
+    const int tid = threadIdx.x;
+    auto loadQ = [&](int k, double* dst) {
+        const double* q = Qbuf + (long)k * BJ2 * BJ2;
+        for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) dst[(e / BJ2) * BJL + e % BJ2] = q[e];
+    };
+    if ((int)blockIdx.x < ntA) {
+        int t = blockIdx.x, I = 0;
+        while (t >= np - I) {
+            t -= np - I;
+            ++I;
+        }
+        const int J = I + t;
+        int ia, ib, ja, jb;
+        round_pair(r, I, nb, ia, ib);
+        round_pair(r, J, nb, ja, jb);
+        for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+            const int lr = e % BJ2, lc = e / BJ2;
+            X[lc * BJL + lr] = W[(long)bj_global(lc, ja, jb) * ld + bj_global(lr, ia, ib)];
+        }
+        loadQ(I, QI);
+        loadQ(J, QJ);
+        __syncthreads();
+        bj_mm<false>(X, QJ, T);  // T = X Q_J
+        __syncthreads();
+        bj_mm<true>(QI, T, X);   // X = Q_I^T T
+        __syncthreads();
+        for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+            const int lr = e % BJ2, lc = e / BJ2;
+            const double v = X[lc * BJL + lr];
+            W[(long)bj_global(lc, ja, jb) * ld + bj_global(lr, ia, ib)] = v;
+        }
+        if (I != J)
+            for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+                const int lr = e % BJ2, lc = e / BJ2;  // element (lr of J-set, lc of I-set)
+                W[(long)bj_global(lc, ia, ib) * ld + bj_global(lr, ja, jb)] = X[lr * BJL + lc];
+            }
+    } else {
+        const int v = blockIdx.x - ntA;
+        const int rt = v % (P / BJ2), J = v / (P / BJ2);
+        int ja, jb;
+        round_pair(r, J, nb, ja, jb);
+        const int r0 = rt * BJ2;
+        for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+            const int lr = e % BJ2, lc = e / BJ2;
+            X[lc * BJL + lr] = V[(long)bj_global(lc, ja, jb) * ldv + r0 + lr];
+        }
+        loadQ(J, QJ);
+        __syncthreads();
+        bj_mm<false>(X, QJ, T);
+        __syncthreads();
+        for (int e = tid; e < BJ2 * BJ2; e += blockDim.x) {
+            const int lr = e % BJ2, lc = e / BJ2;
+            V[(long)bj_global(lc, ja, jb) * ldv + r0 + lr] = T[lc * BJL + lr];
+        }
+    }
+}
+
+__global__ void bj_prepare_kernel(const double* __restrict__ A, long lda, int p, int P,
+                                  double* __restrict__ W, double* __restrict__ V) {
+    const long total = (long)P * P;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e / P), i = (int)(e - (long)j * P);
+        W[e] = (i < p && j < p) ? A[(long)j * lda + i] : 0.0;
+        V[e] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+int block_jacobi_eig(const double* A, long lda, int p, int P, double fro, double* W, double* V,
+                     double* Qbuf, double* vals, double* Vout, long ldo,
+                     unsigned long long* counters, unsigned long long* h_counter, int max_sweeps,
+                     int* sweeps_out, cudaStream_t s) {
+    if (p <= 0) return 0;
+    if (P % BJ2 != 0 || P < p) return -1;
+    const int nb = P / BJ;
+    const int np = nb / 2;
+    const double thr = fro > 0.0 ? 2.220446049250313e-16 * fro : 0.0;
+    bj_prepare_kernel<<<148, 256, 0, s>>>(A, lda, p, P, W, V);
+    const size_t sm_in = sizeof(double) * 2 * BJ2 * BJL;
+    const size_t sm_up = sizeof(double) * 4 * BJ2 * BJL;
+    ensure_smem((const void*)bj_inner_kernel, sm_in);
+    ensure_smem((const void*)bj_update_kernel, sm_up);
+    const int ntiles = np * (np + 1) / 2 + (P / BJ2) * np;
+    // a single pair (P = 64) is the whole problem: iterate it to convergence
+    const int max_inner = np == 1 ? max_sweeps : 1;
+    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * max_sweeps, s);
+    int sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        for (int r = 0; r < nb - 1; ++r) {
+            bj_inner_kernel<<<np, 256, sm_in, s>>>(W, P, nb, r, thr, max_inner, Qbuf,
+                                                   counters + sweep);
+            bj_update_kernel<<<ntiles, 256, sm_up, s>>>(W, P, V, P, P, nb, r, Qbuf);
+        }
+        cudaMemcpyAsync(h_counter, counters + sweep, sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+        if (*h_counter == 0) {
+            ++sweep;
+            break;
+        }
+    }
+    if (sweeps_out) *sweeps_out = sweep;
+    eig_sort_kernel<<<p, 256, 0, s>>>(W, P, p, V, P, vals, Vout, ldo);
+    return 0;
+}
+
 }  // namespace fl
 
 namespace fl {

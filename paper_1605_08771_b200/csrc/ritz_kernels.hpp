@@ -27,6 +27,15 @@ int jacobi_eig(double* A, long lda, int p, double fro, double* work, double* V, 
                double* vals, double* Vout, long ldo, int* scratch_int, unsigned long long* counters,
                int max_sweeps, cudaStream_t s);
 
+// Block-Jacobi symmetric eigensolve of the p x p matrix A (ld lda, left
+// unchanged): P = round_up(p, 64); W, V are P x P (ld P) scratch, Qbuf holds
+// P x 64 doubles; ascending vals[p] and eigenvectors Vout (ld ldo). Host-driven
+// sweeps (one stream synchronisation per sweep via the pinned h_counter).
+int block_jacobi_eig(const double* A, long lda, int p, int P, double fro, double* W, double* V,
+                     double* Qbuf, double* vals, double* Vout, long ldo,
+                     unsigned long long* counters, unsigned long long* h_counter, int max_sweeps,
+                     int* sweeps_out, cudaStream_t s);
+
 // In-place column-pivoted Householder QR (dgeqp3 semantics) of the n x p matrix
 // A; tau[min(n,p)], jpvt[p], norm scratch vn1/vn2[p]. Returns 0 on success.
 int launch_qr(double* A, long lda, int n, int p, double* tau, int* jpvt, double* vn1, double* vn2,

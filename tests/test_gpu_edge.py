@@ -90,3 +90,35 @@ def test_singular_node_device_path_is_raised_at_next_sync():
         ctx.sync()
     assert "singular factorization at node 0" in str(ei.value)
     ctx.sync()  # the verdict is consumed once
+
+
+def test_context_outlives_its_objects_in_any_destruction_order():
+    """fl_ctx is reference counted by its matrices, blocks and filters: the
+    owner may destroy it first (as a garbage collector breaking a cycle may)
+    and the objects stay usable until they are destroyed themselves."""
+    import ctypes as C
+    import paper_1605_08771_b200 as P
+    from paper_1605_08771_b200 import _lib as L
+    lib = L.lib()
+    n, p = 96, 8
+    A = np.asfortranarray(np.diag(np.linspace(-1, 1, n)))
+    X = np.asfortranarray(np.random.default_rng(0).standard_normal((n, p)))
+    ctx, mat, flt, blk = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    err = L.Err()
+    assert lib.fl_ctx_create(0, C.byref(ctx), C.byref(err)) == 0
+    assert lib.fl_matrix_create(ctx, A.ctypes.data, n, n, L.FL_HOST, C.byref(mat), C.byref(err)) == 0
+    rule = P.build_contour_rule(P.SearchInterval(-0.5, 0.5), 4)
+    zr, zi, wr, wi = (np.ascontiguousarray(v) for v in rule.parts())
+    assert lib.fl_filter_create(ctx, mat, 4, zr.ctypes.data, zi.ctypes.data, wr.ctypes.data,
+                                wi.ctypes.data, 0, C.byref(flt), C.byref(err)) == 0
+    assert lib.fl_block_create(ctx, n, p, C.byref(blk), C.byref(err)) == 0
+    assert lib.fl_ctx_destroy(ctx) == 0          # owner gone first
+    Y = np.zeros((n, p), order="F")
+    rhs, facts = C.c_longlong(), C.c_longlong()
+    assert lib.fl_filter_apply_raw(flt, X.ctypes.data, n, p, Y.ctypes.data, n, L.FL_HOST,
+                                   C.byref(rhs), C.byref(facts), C.byref(err)) == 0, err.msg
+    Yo = O.apply_filter(A, O.build_contour_rule(O.SearchInterval(-0.5, 0.5), 4), X)
+    assert np.linalg.norm(Y - Yo) <= 1e-12 * np.linalg.norm(Yo)
+    assert lib.fl_block_destroy(blk) == 0
+    assert lib.fl_filter_destroy(flt) == 0
+    assert lib.fl_matrix_destroy(mat) == 0       # last reference: context torn down here
