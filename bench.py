@@ -270,10 +270,12 @@ def run_b200(args, rank, world, local_rank):
     l0 = ctx.launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects this region
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     e1.synchronize()
     launches = ctx.launches() - l0
     ms = e0.elapsed_time(e1)
@@ -339,6 +341,18 @@ def run_b200(args, rank, world, local_rank):
         return
     mode = P.zgemm_mode()
     zms, zflops, zl = prof["zgemm"]
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # capture of this workload (profiles/), when one exists for it
+    traffic, traffic_src = None, None
+    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                      f"ncu_zgemm_traffic_cfg{args.config}_r01.json")
+    if os.path.exists(tp) and mode == "3m":
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = round(tj["zgemm_sub"]["dram_bytes_per_launch"])
+        traffic_src = (f"{os.path.relpath(tp, os.path.dirname(os.path.abspath(__file__)))}: "
+                       f"dram__bytes_read.sum + dram__bytes_write.sum per zgemm3m SUB launch "
+                       f"(mean of {tj['zgemm_sub']['launches']})")
     total_ms_prof = sum(v[0] for v in prof.values())
     achieved = zflops / (zms * 1e-3) / 1e12 if zms > 0 else 0.0
     cpu = None
@@ -371,7 +385,8 @@ def run_b200(args, rank, world, local_rank):
                                                / FP64_DMMA_PEAK_TFLOPS, 4),
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
-                     "traffic": None,
+                     "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": "measured FP64 DMMA burst, tools/fp64_peak.cu "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
                      "share_of_step": round(zms / ms_serial, 4) if ms_serial else None,

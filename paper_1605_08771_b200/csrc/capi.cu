@@ -701,6 +701,8 @@ void device_sym_eig(fl_ctx* ctx, double* M, long ldm, int p, int P, double* vals
                                         reinterpret_cast<unsigned long long*>(ctx->cnt.p),
                                         ctx->h_cnt, 40, &sweeps, ctx->stream);
         g_launch_count += 2 + 2LL * sweeps * (P / 32 - 1);
+        static const bool dbg = std::getenv("FEASTLAB_EIG_DEBUG") != nullptr;
+        if (dbg) std::fprintf(stderr, "block_jacobi_eig: p=%d sweeps=%d\n", p, sweeps);
         if (rc != 0) throw Fail{FL_CUDA, "block_jacobi_eig failed"};
         CK(cudaGetLastError());
         return;
