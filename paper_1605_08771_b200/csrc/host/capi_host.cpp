@@ -1,6 +1,8 @@
 // Host-level C ABI entry points (include/feastlab_b200.h, bottom section):
 // the drop-in C++ drivers and contour helpers exported for foreign callers.
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -64,7 +66,11 @@ int fl_solve(fl_ctx* ctx, int variant, const double* A, int n, int lda, double l
     return guarded(err, [&] {
         if (n < 1 || lda < n) throw std::invalid_argument("fl_solve: bad matrix shape");
         ScopedContext sc(ctx);
+        const auto t0 = std::chrono::steady_clock::now();
         const SymmetricMatrix S(A, n, lda);
+        if (std::getenv("FEASTLAB_TIME"))
+            std::fprintf(stderr, "fl_solve: SymmetricMatrix %.3f s\n",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         SolverConfig cfg;
         cfg.m0 = c->m0;
         cfg.n_c = c->n_c;
@@ -81,9 +87,13 @@ int fl_solve(fl_ctx* ctx, int variant, const double* A, int n, int lda, double l
         struct Reset {
             ~Reset() { detail::keep_first_filtered = false; }
         } reset;
+        const auto t1 = std::chrono::steady_clock::now();
         Solution s = variant == 0   ? feast_solve(S, I, cfg)
                      : variant == 1 ? xfeast_solve(S, I, cfg)
                                     : rfeast_solve(S, I, cfg);
+        if (std::getenv("FEASTLAB_TIME"))
+            std::fprintf(stderr, "fl_solve: driver %.3f s\n",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count());
         const int k = s.eigenvalues.size();
         *m = k;
         std::memcpy(values, s.eigenvalues.data(), sizeof(double) * k);

@@ -107,11 +107,11 @@ void panel_profile(double* out8, bool reset) {
     }
 }
 
-template <int W, int ROWS, int NT>
+template <int W, int ROWS, int NT, int CL>
 // 256-thread variants are capped at 128 registers so a panel CTA fits on an SM
 // beside one DMMA GEMM CTA: the look-ahead panel then overlaps the trailing
 // update instead of waiting for a fully drained SM.
-__global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 : 1)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 : 1)
     panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char raw[];
@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2
     const long ld = F.ld;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     constexpr int NW = NT / 32;
-    const int R = (N - k0 + PCL2 - 1) / PCL2;  // rows per CTA (<= ROWS * NT)
+    const int R = (N - k0 + CL - 1) / CL;  // rows per CTA (<= ROWS * NT)
     const int base = k0 + rank * R;
     const int top = min(N, base + R);
     auto at = [&](int r, int c) { return (long)c * ld + r; };
@@ -227,7 +227,7 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2
             if (wid == 0) {
                 double s2 = -1.0;
                 int i2 = 0x7fffffff, rk = lane;
-                if (lane < PCL2) {
+                if (lane < CL) {
                     RegPanelShared<W>* rs = cluster.map_shared_rank(&sh, lane);
                     s2 = rs->cand_score[par];
                     i2 = rs->cand_row[par];
@@ -432,19 +432,21 @@ __global__ void __cluster_dims__(PCL2, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2
     cluster.sync();  // shared memory stays alive until every CTA is done with it
 }
 
-template <int W, int ROWS, int NT>
+template <int W, int ROWS, int NT, int CL = PCL2>
 static void launch_reg(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
     const size_t sm = sizeof(RegPanelShared<W>);
-    ensure_smem((const void*)panel_reg_kernel<W, ROWS, NT>, sm);
-    panel_reg_kernel<W, ROWS, NT><<<dim3(PCL2, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab);
+    ensure_smem((const void*)panel_reg_kernel<W, ROWS, NT, CL>, sm);
+    panel_reg_kernel<W, ROWS, NT, CL><<<dim3(CL, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab);
 }
 
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
     const int R = (N - k0 + PCL2 - 1) / PCL2;
+    // smaller leaves than rows allow: the column step is latency-bound, so
+    // W mostly sets the register-select cost (no spills in these shapes)
     if (R <= 256)
-        launch_reg<16, 1, 256>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<8, 1, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 512)
-        launch_reg<8, 2, 256>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 2, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 1024)
         launch_reg<4, 4, 256>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 2048)
