@@ -86,6 +86,15 @@ long long fl_ctx_launches(const fl_ctx* ctx);
 int fl_ctx_set_profiling(fl_ctx* ctx, int on);
 /* number of contour-node chunks factored/solved concurrently (1..4, default 4) */
 int fl_ctx_set_streams(fl_ctx* ctx, int n);
+/* how a multi-rank context combines the per-rank partial filters into Y:
+   FL_REDUCE_SUM (default): local ascending-k sum, then ncclAllReduce(sum) —
+   one n x p exchange, rounding depends on the rank count;
+   FL_REDUCE_ORDERED: all-gather of the per-node terms Re(w_k W_k), then every
+   rank sums all n_c terms in ascending k (filterop.cpp:65-81 / SPEC.md:249) —
+   n_c x n x p bytes exchanged, Y bitwise identical at every GPU count.
+   Single-rank contexts ignore it. */
+enum { FL_REDUCE_SUM = 0, FL_REDUCE_ORDERED = 1 };
+int fl_ctx_set_reduction(fl_ctx* ctx, int mode);
 /* complex product form of the filter's DMMA GEMMs (process-wide): 1 = 3M
    (three real products per complex product, the default), 0 = 4M; mode < 0
    only queries. Returns the mode in effect. Env FEASTLAB_ZGEMM=4m|3m sets

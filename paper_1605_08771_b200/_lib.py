@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("FEASTLAB_LIB") or os.path.join(HERE, "lib", "libfeast
 FL_OK, FL_INVALID_ARGUMENT, FL_RUNTIME_ERROR, FL_CHOLESKY, FL_SINGULAR_NODE, FL_CUDA, FL_NCCL, \
     FL_OOM = range(8)
 FL_HOST, FL_DEVICE = 0, 1
+FL_REDUCE_SUM, FL_REDUCE_ORDERED = 0, 1
 
 _lib = None
 
@@ -59,6 +60,7 @@ _SIGS = {
     "fl_ctx_profile_dump": (_I, [_P, _P, _I]),
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
     "fl_zgemm_mode": (_I, [_I]),
+    "fl_ctx_set_reduction": (_I, [_P, _I]),
     "fl_ctx_profile": (_I, [_P, C.c_char_p, _P, _P, _P, _P]),
     "fl_matrix_create": (_I, [_P, _P, _I, _I, _I, _PP, _P]),
     "fl_matrix_destroy": (_I, [_P]),

@@ -148,6 +148,7 @@ struct fl_ctx {
     std::vector<cudaStream_t> paux;  // per chunk: look-ahead panel stream (high priority)
     std::vector<cudaEvent_t> ev_panel, ev_next;
     int nstreams = 4;  // node chunks in flight (<= aux.size())
+    int reduction = 0;  // FL_REDUCE_SUM / FL_REDUCE_ORDERED (multi-rank Y)
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
         scal;
@@ -186,15 +187,17 @@ struct fl_filter {
     long w_stride = 0;
     int w_P = 0;
     DBuf y_tmp;
+    DBuf terms, terms_all;  // ordered reduction: local / gathered Re(w_k W_k)
     // CUDA graph of one whole application (non-cache mode): captured on the
     // second call with an unchanged launch key, replayed while it holds
     struct GraphKey {
         const void *X, *Y, *fac, *w;
         long ldx, ldy;
-        int p, slots, ns, zmode;
+        int p, slots, ns, zmode, reduction;
         bool operator==(const GraphKey& o) const {
             return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
-                   ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns && zmode == o.zmode;
+                   ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns &&
+                   zmode == o.zmode && reduction == o.reduction;
         }
     };
     GraphKey gkey{}, gseen{};
@@ -305,6 +308,11 @@ struct Prof {
         }
     }
 };
+
+double* scratch(DBuf& b, size_t doubles) {
+    b.ensure(sizeof(double) * std::max<size_t>(doubles, 1));
+    return b.d();
+}
 
 // --------------------------------------------------------------- filter core
 // Factor nodes [g0, g0+G) of the local range into factor slots [s0, s0+G).
@@ -575,13 +583,40 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             w.zi[b] = f->wi[f->kb + b];
         }
         ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
-        if (L > 0) {
+        if (ctx->comm && ctx->reduction == FL_REDUCE_ORDERED) {
+            // every rank's terms at slot rank * Lmax + local index; all-gather;
+            // ascending global-k sum on every rank (bitwise G-invariant)
+            if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "ordered reduction needs a packed Y"};
+            const int G = ctx->nranks;
+            const int Lmax = (f->nc + G - 1) / G;
+            const long ts = (long)N * P;
+            double* T = scratch(f->terms, (size_t)std::max(Lmax, 1) * ts);
+            double* Tall = scratch(f->terms_all, (size_t)G * std::max(Lmax, 1) * ts);
+            NodeSlots sl{};
+            for (int r = 0; r < G; ++r) {
+                int b0 = 0, b1 = 0;
+                fl_node_shard(f->nc, r, G, &b0, &b1);
+                for (int k = b0; k < b1; ++k) sl.slot[k] = r * Lmax + (k - b0);
+            }
+            {
+                Prof pr(ctx, P_ACCUM, 24.0 * L * N * P);
+                launch_node_terms(W, N, P, w, L, T, ts, ctx->stream);
+            }
+            Prof pr(ctx, P_ALLREDUCE, 8.0 * G * Lmax * ts, 1);
+            nccl_check(ncclAllGather(T, Tall, (size_t)Lmax * ts, ncclFloat64, ctx->comm,
+                                     ctx->stream),
+                       "ncclAllGather(node terms)");
+            launch_ordered_sum(Tall, ts, sl, f->nc, N, P, Y, ldy, ctx->stream);
+            nccl_check(ncclAllReduce(f->bad.p, f->bad.p, 1, ncclInt32, ncclMin, ctx->comm,
+                                     ctx->stream),
+                       "ncclAllReduce(bad node)");
+        } else if (L > 0) {
             Prof pr(ctx, P_ACCUM, (16.0 * L + 8.0) * N * P);
             launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
         } else {
             CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
         }
-        if (ctx->comm) {
+        if (ctx->comm && ctx->reduction != FL_REDUCE_ORDERED) {
             if (ldy != N) throw Fail{FL_INVALID_ARGUMENT, "allreduce needs a packed Y"};
             Prof pr(ctx, P_ALLREDUCE, 8.0 * N * p, 0);
             nccl_check(ncclAllReduce(Y, Y, (size_t)N * p, ncclFloat64, ncclSum, ctx->comm,
@@ -594,7 +629,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         }
     };
     const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
-                                  zgemm_mode()};
+                                  zgemm_mode(), ctx->reduction};
     const bool graphable = !f->cache && !ctx->prof.on && graphs_enabled();
     if (graphable && f->gexec && f->gkey == key) {
         CK(cudaGraphLaunch(f->gexec, ctx->stream));
@@ -676,10 +711,6 @@ void resolve_pending(fl_ctx* ctx) {
 }
 
 // --------------------------------------------------------------- Rayleigh-Ritz helpers
-double* scratch(DBuf& b, size_t doubles) {
-    b.ensure(sizeof(double) * std::max<size_t>(doubles, 1));
-    return b.d();
-}
 
 // Symmetric eigensolve of the p x p matrix M (device, ld ldm, destroyed):
 // ascending vals (device), vectors into V (P x P zero-padded, ld P).
@@ -1107,6 +1138,13 @@ int fl_debug_zgemm(fl_ctx* ctx, int M, int Nc, int K, int batch, int iters, doub
         cudaEventDestroy(e1);
         *ms_out = ms / iters;
     });
+}
+
+int fl_ctx_set_reduction(fl_ctx* ctx, int mode) {
+    if (!ctx || (mode != FL_REDUCE_SUM && mode != FL_REDUCE_ORDERED)) return FL_INVALID_ARGUMENT;
+    CtxLock lk(ctx);
+    ctx->reduction = mode;
+    return FL_OK;
 }
 
 int fl_zgemm_mode(int mode) {

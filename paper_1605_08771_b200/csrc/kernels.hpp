@@ -72,6 +72,15 @@ void launch_permute_rhs(const double* X, long ldx, int N, int P, const int* perm
 // Y (+)= sum_{b ascending} Re(w_b W_b): Y = beta*Y + sum (beta in {0,1}).
 void launch_accumulate(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* Y, long ldy,
                        bool add_to_Y, cudaStream_t s);
+// G-invariant reduction: T[b] = Re(w_b W_b) (tstride apart), then on every
+// rank Y = sum over global nodes k ascending of T[slot[k]].
+struct NodeSlots {
+    int slot[kMaxNodes];
+};
+void launch_node_terms(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* T,
+                       long tstride, cudaStream_t s);
+void launch_ordered_sum(const double* T, long tstride, const NodeSlots& sl, int nc, int N, int P,
+                        double* Y, long ldy, cudaStream_t s);
 // |U_ii| > 0 and finite for all i < n; on failure atomicMin(bad_node, offset + b).
 void launch_check_diag(ZBatch F, int n, int batch, int offset, int* bad_node, cudaStream_t s);
 

@@ -271,6 +271,48 @@ void launch_accumulate(ZBatch W, int N, int P, const NodeShifts& w, int batch, d
     accumulate_kernel<<<148 * 4, 256, 0, s>>>(W, N, P, w, batch, Y, ldy, add_to_Y);
 }
 
+// G-invariant reduction (fl_ctx_set_reduction ORDERED): every rank writes its
+// nodes' terms t_b = Re(w_b W_b) (the same two rounded products and rounded
+// difference as accumulate_kernel); after an all-gather every rank sums all
+// n_c terms in ascending global node order, which is accumulate_kernel's
+// association on one GPU: Y is bitwise the same at every GPU count.
+__global__ void node_terms_kernel(ZBatch W, int N, int P, NodeShifts w, int batch, double* T,
+                                  long tstride) {
+    const long total = (long)N * P;
+    const int b = blockIdx.y;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e / N, r = e - c * N;
+        const long o = b * W.stride + c * W.ld + r;
+        T[b * tstride + e] = __dsub_rn(__dmul_rn(w.zr[b], W.re[o]), __dmul_rn(w.zi[b], W.im[o]));
+    }
+}
+
+__global__ void ordered_sum_kernel(const double* __restrict__ T, long tstride, NodeSlots sl, int nc,
+                                   int N, int P, double* Y, long ldy) {
+    const long total = (long)N * P;
+    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long c = e / N, r = e - c * N;
+        double y = 0.0;
+        for (int k = 0; k < nc; ++k) y = __dadd_rn(y, T[sl.slot[k] * tstride + e]);
+        Y[c * ldy + r] = y;
+    }
+}
+
+void launch_node_terms(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* T,
+                       long tstride, cudaStream_t s) {
+    if (P <= 0 || batch <= 0) return;
+    node_terms_kernel<<<dim3(148 * 4 / batch + 1, batch), 256, 0, s>>>(W, N, P, w, batch, T,
+                                                                       tstride);
+}
+
+void launch_ordered_sum(const double* T, long tstride, const NodeSlots& sl, int nc, int N, int P,
+                        double* Y, long ldy, cudaStream_t s) {
+    if (P <= 0) return;
+    ordered_sum_kernel<<<148 * 4, 256, 0, s>>>(T, tstride, sl, nc, N, P, Y, ldy);
+}
+
 // ------------------------------------------------------------------ singularity check
 __global__ void check_diag_kernel(ZBatch F, int n, int offset, int* bad_node) {
     const int b = blockIdx.y;

@@ -117,6 +117,14 @@ class Context:
         """Contour-node chunks in flight (1 serialises the filter's kernels)."""
         L.lib().fl_ctx_set_streams(self.handle, int(n))
 
+    def set_reduction(self, mode: str) -> None:
+        """Multi-rank combination of the partial filters: "sum" (all-reduce,
+        default) or "ordered" (all-gather + ascending-k sum: Y bitwise the same
+        at every GPU count)."""
+        if mode not in ("sum", "ordered"):
+            raise InvalidArgument("set_reduction: mode must be 'sum' or 'ordered'")
+        _check(L.lib().fl_ctx_set_reduction(self.handle, 1 if mode == "ordered" else 0), L.Err())
+
     def set_profiling(self, on: bool) -> None:
         """Per-kernel-class CUDA-event timing on the context stream."""
         L.lib().fl_ctx_set_profiling(self.handle, int(bool(on)))

@@ -81,3 +81,14 @@ def test_compute_entry_fails_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(P.FeastCudaError):
         P.apply_filter(np.eye(4), P.build_contour_rule(P.SearchInterval(-1, 1), 2), np.ones((4, 1)))
+
+
+def test_library_then_torch_import_order():
+    """Loading the library before torch must not pin an NCCL older than the
+    one torch needs (the library links torch's NCCL when it is installed)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1605_08771_b200; import torch; "
+            "print('ok')" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]

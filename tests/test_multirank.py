@@ -79,3 +79,68 @@ def test_two_rank_sharded_filter_sum_gloo():
     status, val = q.get(timeout=10)
     assert status == "ok", val
     assert val <= 1e-13
+
+
+def _ordered_worker(rank, world, port, out):
+    """FL_REDUCE_ORDERED host logic (capi.cu filter_apply_dev): rank r writes
+    its nodes' terms Re(w_k W_k) at slots r*Lmax + (k - kb), the slots are
+    all-gathered, every rank sums the n_c terms in ascending global k."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+
+        import oracle as O
+        from paper_1605_08771_b200 import dist as D
+        n, p, nc = 36, 4, 8
+        A = O.random_symmetric(n, 91) / np.sqrt(n)
+        X = O.random_block(n, p, 92)
+        rule = O.build_contour_rule(O.SearchInterval(-0.4, 0.6), nc)
+        z = np.asarray(rule.nodes)
+        w = np.asarray(rule.weights)
+
+        def term(k):  # Re(w W) as two rounded products and a rounded difference
+            W = O.node_solve(A, z[k], X)
+            return w[k].real * W.real - w[k].imag * W.imag
+
+        Lmax = -(-nc // world)
+        kb, ke = D.node_shard(nc, rank, world)
+        local = np.zeros((Lmax, n, p))
+        for k in range(kb, ke):
+            local[k - kb] = term(k)
+        gathered = [torch.zeros(Lmax, n, p, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(local))
+        slots = {}
+        for r in range(world):
+            b0, b1 = D.node_shard(nc, r, world)
+            for k in range(b0, b1):
+                slots[k] = (r, k - b0)
+        Y = np.zeros((n, p))
+        for k in range(nc):  # ascending global order
+            r, i = slots[k]
+            Y = Y + gathered[r][i].numpy()
+        single = np.zeros((n, p))
+        for k in range(nc):
+            single = single + term(k)
+        if rank == 0:
+            out.put(("ok", bool(np.array_equal(Y, single))))
+    except Exception as e:
+        out.put(("err", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ordered_reduction_is_bitwise_rank_invariant_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ordered_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(180)
+    status, val = q.get(timeout=10)
+    assert status == "ok", val
+    assert val is True
