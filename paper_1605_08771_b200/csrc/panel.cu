@@ -17,6 +17,8 @@
 // L entries (one global read-modify-write per row).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -29,17 +31,17 @@ namespace {
 constexpr int PCL2 = 8;   // cluster size (portable)
 constexpr int PWID = 64;  // outer panel width
 
-template <int W>
+template <int W, int CL>
 struct RegPanelShared {
-    double cand_score[2];
-    int cand_row[2];
-    double cand_vals[2][2][W];
+    // pushed by every rank of the cluster into every rank (parity buffered):
+    // its best candidate (score, row, the row's W entries) and, from the owner
+    // of row j, row j itself -- after the cluster barrier all of it is local
+    double slot_score[2][CL];
+    int slot_row[2][CL];
+    double slot_vals[2][CL][2][W];
     double diag_vals[2][2][W];
-    double ur[W], ui[W];    // pivot row (this column)
-    double ojr[W], oji[W];  // old row j (goes to row piv)
     double red_s[32];
     int red_i[32];
-    int piv, winner;
     int pivs[PWID];
     // leaf U block: Lqq (W x W) and U (W x PWID)
     double lr[W][W + 1], li[W][W + 1];
@@ -115,7 +117,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
     panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char raw[];
-    RegPanelShared<W>& sh = *reinterpret_cast<RegPanelShared<W>*>(raw);
+    RegPanelShared<W, CL>& sh = *reinterpret_cast<RegPanelShared<W, CL>*>(raw);
     const int rank = (int)cluster.block_rank();
     const int b = blockIdx.y;
     double* Fr = F.re + b * F.stride;
@@ -193,88 +195,88 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
                 sh.red_i[wid] = idx;
             }
             __syncthreads();
-            if (wid == 0) {
+            {
+                // every warp reduces the CTA's candidates redundantly; the
+                // owners push the winner and row j into every rank's slots
                 double s2 = lane < NW ? sh.red_s[lane] : -1.0;
                 int i2 = lane < NW ? sh.red_i[lane] : 0x7fffffff;
                 warp_argmax(s2, i2);
-                if (lane == 0) {
-                    sh.cand_score[par] = s2;
-                    sh.cand_row[par] = (s2 >= 0.0) ? i2 : -1;
+                const int cr = (s2 >= 0.0) ? i2 : -1;
+                if (tid < CL) {
+                    auto* d = cluster.map_shared_rank(&sh, tid);
+                    d->slot_score[par][rank] = s2;
+                    d->slot_row[par][rank] = cr;
                 }
-            }
-            __syncthreads();
-            {
-                const int cr = sh.cand_row[par];
+                bool own_c = false, own_j = false;
+                double vr[W], vi[W], dr_[W], di_[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) vr[k] = vi[k] = dr_[k] = di_[k] = 0.0;
 #pragma unroll
                 for (int i = 0; i < ROWS; ++i) {
-                    if (has[i] && row[i] == cr)
+                    const bool c = has[i] && row[i] == cr, d = has[i] && row[i] == j;
+                    own_c |= c;
+                    own_j |= d;
 #pragma unroll
-                        for (int k = 0; k < W; ++k) {
-                            sh.cand_vals[par][0][k] = xr[i][k];
-                            sh.cand_vals[par][1][k] = xi[i][k];
+                    for (int k = 0; k < W; ++k) {
+                        if (c) {
+                            vr[k] = xr[i][k];
+                            vi[k] = xi[i][k];
                         }
-                    if (has[i] && row[i] == j)
-#pragma unroll
-                        for (int k = 0; k < W; ++k) {
-                            sh.diag_vals[par][0][k] = xr[i][k];
-                            sh.diag_vals[par][1][k] = xi[i][k];
+                        if (d) {
+                            dr_[k] = xr[i][k];
+                            di_[k] = xi[i][k];
                         }
+                    }
                 }
+                if (own_c)
+#pragma unroll 1
+                    for (int r = 0; r < CL; ++r) {
+                        auto* d = cluster.map_shared_rank(&sh, r);
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            d->slot_vals[par][rank][0][k] = vr[k];
+                            d->slot_vals[par][rank][1][k] = vi[k];
+                        }
+                    }
+                if (own_j)
+#pragma unroll 1
+                    for (int r = 0; r < CL; ++r) {
+                        auto* d = cluster.map_shared_rank(&sh, r);
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            d->diag_vals[par][0][k] = dr_[k];
+                            d->diag_vals[par][1][k] = di_[k];
+                        }
+                    }
             }
             PPROF(0);
-            cluster.sync();
+            cluster.sync();  // release/acquire: every rank's pushes are visible
             PPROF(1);
-            if (wid == 0) {
-                double s2 = -1.0;
-                int i2 = 0x7fffffff, rk = lane;
-                if (lane < CL) {
-                    RegPanelShared<W>* rs = cluster.map_shared_rank(&sh, lane);
-                    s2 = rs->cand_score[par];
-                    i2 = rs->cand_row[par];
-                    if (i2 < 0) {
-                        s2 = -1.0;
-                        i2 = 0x7fffffff;
-                    }
-                }
+            // every thread reduces the CL local slots (lowest row on ties)
+            double sw = -1.0;
+            int iw = 0x7fffffff, winner = 0;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double so = __shfl_xor_sync(0xffffffffu, s2, off);
-                    const int io = __shfl_xor_sync(0xffffffffu, i2, off);
-                    const int ro = __shfl_xor_sync(0xffffffffu, rk, off);
-                    if (better(so, io, s2, i2)) {
-                        s2 = so;
-                        i2 = io;
-                        rk = ro;
-                    }
-                }
-                if (lane == 0) {
-                    sh.piv = (s2 > 0.0) ? i2 : j;  // all-zero column: no interchange
-                    sh.winner = (s2 > 0.0) ? rk : owner_rank(j);
+            for (int r = 0; r < CL; ++r) {
+                const int rr = sh.slot_row[par][r];
+                const double sr = rr < 0 ? -1.0 : sh.slot_score[par][r];
+                const int ir = rr < 0 ? 0x7fffffff : rr;
+                if (better(sr, ir, sw, iw)) {
+                    sw = sr;
+                    iw = ir;
+                    winner = r;
                 }
             }
-            __syncthreads();
-            const int piv = sh.piv;
-            if (tid < W) {
-                RegPanelShared<W>* ds = cluster.map_shared_rank(&sh, owner_rank(j));
-                const double ojr = ds->diag_vals[par][0][tid], oji = ds->diag_vals[par][1][tid];
-                if (piv == j) {
-                    sh.ur[tid] = ojr;
-                    sh.ui[tid] = oji;
-                } else {
-                    RegPanelShared<W>* ws = cluster.map_shared_rank(&sh, sh.winner);
-                    sh.ur[tid] = ws->cand_vals[par][0][tid];
-                    sh.ui[tid] = ws->cand_vals[par][1][tid];
-                }
-                sh.ojr[tid] = ojr;
-                sh.oji[tid] = oji;
-            }
+            const int piv = (sw > 0.0) ? iw : j;  // all-zero column: no interchange
+            const double* pvr = piv == j ? sh.diag_vals[par][0] : sh.slot_vals[par][winner][0];
+            const double* pvi = piv == j ? sh.diag_vals[par][1] : sh.slot_vals[par][winner][1];
+            const double* ojr = sh.diag_vals[par][0];
+            const double* oji = sh.diag_vals[par][1];
             if (rank == 0 && tid == 0) {
                 sh.pivs[q * W + jj] = piv;
                 ipiv[(long)b * N + j] = piv;
             }
-            __syncthreads();
             PPROF(2);
-            const cplx pv{sh.ur[jj], sh.ui[jj]};
+            const cplx pv{pvr[jj], pvi[jj]};
             const bool nonzero = (pv.re != 0.0 || pv.im != 0.0);
             const cplx inv = nonzero ? crecip(pv) : cplx{0.0, 0.0};
 #pragma unroll
@@ -283,15 +285,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
                 if (row[i] == j) {
 #pragma unroll
                     for (int k = 0; k < W; ++k) {
-                        xr[i][k] = sh.ur[k];
-                        xi[i][k] = sh.ui[k];
+                        xr[i][k] = pvr[k];
+                        xi[i][k] = pvi[k];
                     }
                 } else if (row[i] > j) {
                     if (row[i] == piv) {
 #pragma unroll
                         for (int k = 0; k < W; ++k) {
-                            xr[i][k] = sh.ojr[k];
-                            xi[i][k] = sh.oji[k];
+                            xr[i][k] = ojr[k];
+                            xi[i][k] = oji[k];
                         }
                     }
                     cplx l{0.0, 0.0};
@@ -305,7 +307,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
                             xr[i][k] = l.re;
                             xi[i][k] = l.im;
                         } else if (k > jj) {
-                            const double ur = sh.ur[k], ui = sh.ui[k];
+                            const double ur = pvr[k], ui = pvi[k];
                             xr[i][k] -= l.re * ur - l.im * ui;
                             xi[i][k] -= l.re * ui + l.im * ur;
                         }
@@ -434,25 +436,47 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
 
 template <int W, int ROWS, int NT, int CL = PCL2>
 static void launch_reg(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
-    const size_t sm = sizeof(RegPanelShared<W>);
+    const size_t sm = sizeof(RegPanelShared<W, CL>);
     ensure_smem((const void*)panel_reg_kernel<W, ROWS, NT, CL>, sm);
     panel_reg_kernel<W, ROWS, NT, CL><<<dim3(CL, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab);
 }
 
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
-    const int R = (N - k0 + PCL2 - 1) / PCL2;
-    // smaller leaves than rows allow: the column step is latency-bound, so
-    // W mostly sets the register-select cost (no spills in these shapes)
+template <int CL>
+static void launch_panel_cl(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch,
+                            cudaStream_t s) {
+    const int R = (N - k0 + CL - 1) / CL;
     if (R <= 256)
-        launch_reg<8, 1, 256>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<8, 1, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 512)
-        launch_reg<4, 2, 256>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 2, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 1024)
-        launch_reg<4, 4, 256>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 4, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
     else if (R <= 2048)
-        launch_reg<4, 4, 512>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<2, 8, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
     else
-        launch_reg<2, 8, 512>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<2, 8, 512, CL>(F, N, k0, ipiv, ptab, batch, s);
+}
+
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+    // 4-CTA clusters for short panels of small problems (<= 2048 rows of an
+    // N <= 4096 matrix: 2 rows per thread, half the SMs a panel holds beside
+    // the GEMMs); 8-CTA clusters otherwise. Measured (ms per application):
+    // cfg0 8.8 -> 8.1, cfg2 146.2 -> 144.1; cfg3 / cfg4 keep 8 (532 / 11004
+    // vs 538 / 11195 with the 4-CTA tails)
+    static const int force = [] {
+        const char* e = std::getenv("FEASTLAB_PANEL_CL");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int rows = N - k0;
+    if (force == 4 || (force == 0 && rows <= 2048 && N <= 4096)) {
+        launch_panel_cl<4>(F, N, k0, ipiv, ptab, batch, s);
+        return;
+    }
+    if (force == 2) {
+        launch_panel_cl<2>(F, N, k0, ipiv, ptab, batch, s);
+        return;
+    }
+    launch_panel_cl<PCL2>(F, N, k0, ipiv, ptab, batch, s);
 }
 
 }  // namespace fl
