@@ -370,9 +370,8 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         return e ? std::atoi(e) : 0;
     }();
     auto panel = [&](int k, int* tab) {
-        Prof pr(ctx, P_PANEL, 0.0, 2, sp);
-        if (!(dbg_skip & 1)) launch_panel(F, N, k, ipiv, tab, G, sp);
-        if (!(dbg_skip & 2)) launch_trinv(F, k, 1, false, Inv, k / T, G, sp);
+        Prof pr(ctx, P_PANEL, 0.0, 1, sp);  // also writes L_kk^{-1} into Inv
+        if (!(dbg_skip & 1)) launch_panel(F, N, k, ipiv, tab, Inv, G, sp);
     };
     auto swaps = [&](const int* tab, int a0, int a1, int b0, int b1, cudaStream_t s) {
         if (dbg_skip & 4) return;

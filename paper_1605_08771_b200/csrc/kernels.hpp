@@ -52,8 +52,10 @@ struct NodeShifts {
 void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& z, int batch,
                   cudaStream_t s);
 // Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j];
-// ptab[b*257 ...] receives the panel's net row permutation (count, rows, sources).
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s);
+// ptab[b*257 ...] receives the panel's net row permutation (count, rows, sources);
+// Inv block k0/64 (see launch_trinv) receives L_kk^{-1}.
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
+                  cudaStream_t s);
 // Cycle counts of the panel kernel phases (node 0, rank 0, thread 0).
 void panel_profile(double* out8, bool reset);
 // Apply a panel's 64 row interchanges (ptab) to the columns [a0,a1) U [b0,b1).

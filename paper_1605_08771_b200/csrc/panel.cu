@@ -49,6 +49,8 @@ struct RegPanelShared {
     // row permutation scratch (rank 0)
     int tpos[2 * PWID], tsrc[2 * PWID];
     double gr[2 * W][PWID], gi[2 * W][PWID];
+    // L_kk staged for its inverse (column-major, ld PWID + 1)
+    double Lkr[PWID][PWID + 1], Lki[PWID][PWID + 1];
 };
 
 // net permutation of interchanges (first+q, piv[q]) q < count, by one warp;
@@ -114,7 +116,8 @@ template <int W, int ROWS, int NT, int CL>
 // beside one DMMA GEMM CTA: the look-ahead panel then overlaps the trailing
 // update instead of waiting for a fully drained SM.
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 : 1)
-    panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab) {
+    panel_reg_kernel(ZBatch F, int N, int k0, int* __restrict__ ipiv, int* __restrict__ ptab,
+                     ZBatch Inv) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char raw[];
     RegPanelShared<W, CL>& sh = *reinterpret_cast<RegPanelShared<W, CL>*>(raw);
@@ -431,33 +434,69 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
             tab[1 + 2 * PWID + m] = sh.tsrc[m];
         }
     }
+    // ---- L_kk^{-1} (unit lower 64 x 64; the solves and U12 multiply by it):
+    // L_kk is final after the last leaf's interchanges (barrier above). One
+    // warp per column c, axpy form x[k+1:] -= L[k+1:, k] x_k with lane l owning
+    // rows l and l + 32; the next column of L is loaded one step ahead.
+    {
+        double* Ir = Inv.re + b * Inv.stride + (long)(k0 / PWID) * PWID * PWID;
+        double* Ii = Inv.im + b * Inv.stride + (long)(k0 / PWID) * PWID * PWID;
+        for (int e = tid; e < PWID * PWID; e += NT) {
+            const int r = e & (PWID - 1), k = e >> 6;
+            const long o = (long)(k0 + k) * ld + k0 + r;
+            sh.Lkr[k][r] = r > k ? Fr[o] : 0.0;
+            sh.Lki[k][r] = r > k ? Fi[o] : 0.0;
+        }
+        __syncthreads();
+        const int gw = rank * NW + wid;
+        for (int c = gw; c < PWID; c += CL * NW) {
+            double x0r = lane == c ? 1.0 : 0.0, x0i = 0.0;
+            double x1r = lane + 32 == c ? 1.0 : 0.0, x1i = 0.0;
+            for (int k = c; k < PWID - 1; ++k) {
+                const double xkr = __shfl_sync(0xffffffffu, k < 32 ? x0r : x1r, k & 31);
+                const double xki = __shfl_sync(0xffffffffu, k < 32 ? x0i : x1i, k & 31);
+                const double l0r = sh.Lkr[k][lane], l0i = sh.Lki[k][lane];
+                const double l1r = sh.Lkr[k][lane + 32], l1i = sh.Lki[k][lane + 32];
+                x0r -= l0r * xkr - l0i * xki;
+                x0i -= l0r * xki + l0i * xkr;
+                x1r -= l1r * xkr - l1i * xki;
+                x1i -= l1r * xki + l1i * xkr;
+            }
+            Ir[(long)c * PWID + lane] = x0r;
+            Ii[(long)c * PWID + lane] = x0i;
+            Ir[(long)c * PWID + lane + 32] = x1r;
+            Ii[(long)c * PWID + lane + 32] = x1i;
+        }
+    }
     cluster.sync();  // shared memory stays alive until every CTA is done with it
 }
 
 template <int W, int ROWS, int NT, int CL = PCL2>
-static void launch_reg(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+static void launch_reg(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
+                       cudaStream_t s) {
     const size_t sm = sizeof(RegPanelShared<W, CL>);
     ensure_smem((const void*)panel_reg_kernel<W, ROWS, NT, CL>, sm);
-    panel_reg_kernel<W, ROWS, NT, CL><<<dim3(CL, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab);
+    panel_reg_kernel<W, ROWS, NT, CL><<<dim3(CL, batch), NT, sm, s>>>(F, N, k0, ipiv, ptab, Inv);
 }
 
 template <int CL>
-static void launch_panel_cl(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch,
-                            cudaStream_t s) {
+static void launch_panel_cl(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv,
+                            int batch, cudaStream_t s) {
     const int R = (N - k0 + CL - 1) / CL;
     if (R <= 256)
-        launch_reg<8, 1, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<8, 1, 256, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
     else if (R <= 512)
-        launch_reg<4, 2, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 2, 256, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
     else if (R <= 1024)
-        launch_reg<4, 4, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<4, 4, 256, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
     else if (R <= 2048)
-        launch_reg<2, 8, 256, CL>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<2, 8, 256, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
     else
-        launch_reg<2, 8, 512, CL>(F, N, k0, ipiv, ptab, batch, s);
+        launch_reg<2, 8, 512, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
 }
 
-void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cudaStream_t s) {
+void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
+                  cudaStream_t s) {
     // 4-CTA clusters for short panels of small problems (<= 2048 rows of an
     // N <= 4096 matrix: 2 rows per thread, half the SMs a panel holds beside
     // the GEMMs); 8-CTA clusters otherwise. Measured (ms per application):
@@ -469,14 +508,14 @@ void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, int batch, cuda
     }();
     const int rows = N - k0;
     if (force == 4 || (force == 0 && rows <= 2048 && N <= 4096)) {
-        launch_panel_cl<4>(F, N, k0, ipiv, ptab, batch, s);
+        launch_panel_cl<4>(F, N, k0, ipiv, ptab, Inv, batch, s);
         return;
     }
     if (force == 2) {
-        launch_panel_cl<2>(F, N, k0, ipiv, ptab, batch, s);
+        launch_panel_cl<2>(F, N, k0, ipiv, ptab, Inv, batch, s);
         return;
     }
-    launch_panel_cl<PCL2>(F, N, k0, ipiv, ptab, batch, s);
+    launch_panel_cl<PCL2>(F, N, k0, ipiv, ptab, Inv, batch, s);
 }
 
 }  // namespace fl
