@@ -201,6 +201,17 @@ int fl_solve(fl_ctx* ctx, int variant, const double* A, int n, int lda, double l
              int* converged, int* iterations, long long* rhs_solved, long long* factorizations,
              int* recovery_events, fl_trace_record* trace, int* ntrace, double* first_filtered,
              fl_err* err);
+/* Concurrent independent solves on one matrix (extension, SURVEY §8(f)(2):
+   search intervals / the CLI's compare cells, feastlab_cli.cpp:245-294):
+   njobs jobs (variant[j], [lo[j], hi[j]], cfgs[j]) over per_device worker
+   contexts on each of devices[0..ndev-1]. Per job: m[j] eigenvalues into
+   values + j * ldv (ascending; ldv >= max m0), converged[j], iterations[j],
+   max_residual[j] (last trace record), status[j] (FL_OK, or FL_RUNTIME_ERROR for a failed
+   job: its message into errors + j * 256 when errors != NULL). */
+int fl_solve_many(const int* devices, int ndev, int per_device, const double* A, int n, int lda,
+                  int njobs, const int* variant, const double* lo, const double* hi,
+                  const fl_solver_config* cfgs, double* values, int ldv, int* m, int* converged,
+                  int* iterations, double* max_residual, int* status, char* errors, fl_err* err);
 /* contour.hpp:28-56 */
 int fl_gauss_legendre(int n, double* nodes, double* weights, fl_err* err);
 int fl_build_contour_rule(double lo, double hi, int n_c, double* zr, double* zi, double* wr,

@@ -188,6 +188,52 @@ void fl_uniform_fill(double* out, long long count, double lo, double hi, uint64_
 
 }  // extern "C"
 
+int fl_solve_many(const int* devices, int ndev, int per_device, const double* A, int n, int lda,
+                  int njobs, const int* variant, const double* lo, const double* hi,
+                  const fl_solver_config* cfgs, double* values, int ldv, int* m, int* converged,
+                  int* iterations, double* max_residual, int* status, char* errors, fl_err* err) {
+    return guarded(err, [&] {
+        if (n < 1 || lda < n || njobs < 0 || ndev < 0 || (njobs > 0 && ldv < 1))
+            throw std::invalid_argument("fl_solve_many: bad arguments");
+        const SymmetricMatrix S(A, n, lda);
+        std::vector<SolveJob> jobs;
+        for (int j = 0; j < njobs; ++j) {
+            const fl_solver_config* c = cfgs + j;
+            SolverConfig cfg;
+            cfg.m0 = c->m0;
+            cfg.n_c = c->n_c;
+            cfg.s = c->s;
+            cfg.tol = c->tol;
+            cfg.max_iter = c->max_iter;
+            cfg.seed = c->seed;
+            cfg.orthogonalizer = c->orthogonalizer == 1 ? Orthogonalizer::qr : Orthogonalizer::svd;
+            cfg.drop_tol = c->drop_tol;
+            cfg.cache_factorizations = c->cache_factorizations != 0;
+            cfg.generalized_reduced = c->generalized_reduced != 0;
+            jobs.emplace_back(variant[j] == 1   ? SolveVariant::xfeast
+                              : variant[j] == 2 ? SolveVariant::rfeast
+                                                : SolveVariant::feast,
+                              SearchInterval(lo[j], hi[j]), cfg);
+        }
+        std::vector<int> devs(devices, devices + ndev);
+        const std::vector<JobResult> res = solve_concurrently(S, jobs, devs, per_device);
+        for (int j = 0; j < njobs; ++j) {
+            const Solution& sol = res[j].solution;
+            const int k = std::min<int>(static_cast<int>(sol.eigenvalues.size()), ldv);
+            m[j] = k;
+            std::memcpy(values + (size_t)j * ldv, sol.eigenvalues.data(), sizeof(double) * k);
+            converged[j] = sol.converged ? 1 : 0;
+            iterations[j] = sol.iterations;
+            max_residual[j] = sol.trace.records.empty() ? 0.0 : sol.trace.records.back().max_residual;
+            status[j] = res[j].failed ? FL_RUNTIME_ERROR : FL_OK;
+            if (errors) {
+                char* e = errors + (size_t)j * 256;
+                std::snprintf(e, 256, "%s", res[j].error.c_str());
+            }
+        }
+    });
+}
+
 extern "C" int fl_node_shard(int n_c, int rank, int nranks, int* k_begin, int* k_end) {
     if (nranks < 1 || rank < 0 || rank >= nranks || n_c < 0) return FL_INVALID_ARGUMENT;
     *k_begin = static_cast<int>(static_cast<long long>(n_c) * rank / nranks);

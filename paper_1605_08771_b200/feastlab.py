@@ -619,6 +619,46 @@ def rfeast_solve(A, interval, cfg, **kw) -> Solution:
     return _solve(2, A, interval, cfg, **kw)
 
 
+def solve_many(A, jobs, devices=(0,), per_device: int = 4):
+    """Independent solves on one matrix run concurrently (the
+    CLI's compare cells, feastlab_cli.cpp:245-294): jobs = [(variant, interval,
+    cfg)], variant in {"feast", "xfeast", "rfeast"}; `per_device` worker
+    contexts per GPU. Returns per job a dict with eigenvalues, converged,
+    iterations, max_residual and error (None, or the failed job's message)."""
+    S = _as_sym(A)
+    M = S.mat()
+    n = S.dim()
+    nj = len(jobs)
+    names = {"feast": 0, "xfeast": 1, "rfeast": 2}
+    var = np.array([names[j[0]] for j in jobs], dtype=np.int32)
+    lo = np.array([j[1].lo for j in jobs], dtype=np.float64)
+    hi = np.array([j[1].hi for j in jobs], dtype=np.float64)
+    cfgs = (L.SolverConfigC * max(nj, 1))()
+    for k, (_, _, cfg) in enumerate(jobs):
+        cfgs[k] = L.SolverConfigC(cfg.m0, cfg.n_c, cfg.s, cfg.tol, cfg.max_iter, cfg.seed,
+                                  1 if cfg.orthogonalizer == "qr" else 0, cfg.drop_tol,
+                                  int(cfg.cache_factorizations), int(cfg.generalized_reduced))
+    ldv = max([max(j[2].m0, 1) for j in jobs] + [1])
+    vals = np.zeros((max(nj, 1), ldv))
+    m = np.zeros(max(nj, 1), dtype=np.int32)
+    conv = np.zeros_like(m)
+    iters = np.zeros_like(m)
+    res = np.zeros(max(nj, 1))
+    status = np.zeros_like(m)
+    errs = C.create_string_buffer(256 * max(nj, 1))
+    devs = np.array(list(devices), dtype=np.int32)
+    _call(L.lib().fl_solve_many, _ptr(devs), len(devs), int(per_device), _ptr(M), n, n, nj,
+          _ptr(var), _ptr(lo), _ptr(hi), cfgs, _ptr(vals), ldv, _ptr(m), _ptr(conv), _ptr(iters),
+          _ptr(res), _ptr(status), errs)
+    out = []
+    for k in range(nj):
+        err = errs.raw[256 * k: 256 * (k + 1)].split(b"\0", 1)[0].decode(errors="replace")
+        out.append({"eigenvalues": vals[k, : m[k]].copy(), "converged": bool(conv[k]),
+                    "iterations": int(iters[k]), "max_residual": float(res[k]),
+                    "error": err if status[k] else None})
+    return out
+
+
 def write_trace_csv(trace) -> str:
     """proj/src/drivers.cpp:13-21 ("%d,%d,%lld,%.17g,%d")."""
     rows = ["iter,subspace_dim,rhs_cumulative,max_residual,m_found\n"]
