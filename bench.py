@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=8, help="node chunks in flight (1..8)")
     return ap.parse_args()
 
 
@@ -235,6 +236,7 @@ def run_b200(args, rank, world, local_rank):
         dist.init_process_group("gloo")  # rendezvous only; the filter all-reduce is NCCL in-library
     ctx = D.make_context(rank, world, local_rank)
     P.set_default_context(ctx)
+    ctx.set_streams(args.streams)
 
     A, vals, c = build_workload(args.config, local_rank)
     n, p, nc = c["n"], c["m0"], c["n_c"]
@@ -292,7 +294,7 @@ def run_b200(args, rank, world, local_rank):
     ms_serial = e0.elapsed_time(e1)
     prof = {k: ctx.profile(k) for k in P.Context.KERNEL_CLASSES}
     ctx.set_profiling(False)
-    ctx.set_streams(4)
+    ctx.set_streams(args.streams)
     if dist:
         ms = D.max_over_ranks(ms)
     total_flops = filter_flops(n, p, nc) * args.steps

@@ -84,7 +84,7 @@ long long fl_ctx_launches(const fl_ctx* ctx);
    classes "shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
    "allreduce"; work = algorithmic flops (GEMM/TRSM) or bytes (streams). */
 int fl_ctx_set_profiling(fl_ctx* ctx, int on);
-/* number of contour-node chunks factored/solved concurrently (1..4, default 4) */
+/* number of contour-node chunks factored/solved concurrently (1..8, default 8) */
 int fl_ctx_set_streams(fl_ctx* ctx, int n);
 /* how a multi-rank context combines the per-rank partial filters into Y:
    FL_REDUCE_SUM (default): local ascending-k sum, then ncclAllReduce(sum) —

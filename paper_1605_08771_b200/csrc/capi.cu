@@ -147,7 +147,7 @@ struct fl_ctx {
     std::vector<cudaEvent_t> join;
     std::vector<cudaStream_t> paux;  // per chunk: look-ahead panel stream (high priority)
     std::vector<cudaEvent_t> ev_panel, ev_next;
-    int nstreams = 4;  // node chunks in flight (<= aux.size())
+    int nstreams = 8;  // node chunks in flight (<= aux.size())
     int reduction = 0;  // FL_REDUCE_SUM / FL_REDUCE_ORDERED (multi-rank Y)
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
@@ -986,7 +986,7 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         c->device = device;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        const int naux = 4;
+        const int naux = 8;
         int prio_lo = 0, prio_hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         c->aux.resize(naux);
