@@ -1,0 +1,77 @@
+"""cfg3 and cfg4 against their exact spectra (no CPU oracle run: the oracle
+needs ~10 min for cfg3 and hours for cfg4 on the host; both problems have a
+known answer). cfg3: the 96 x 96 Dirichlet Laplacian, analytic eigenpairs
+u_jk(p, q) = sin(j pi p h) sin(k pi q h), 200 inside with degenerate pairs.
+cfg4: A = Q Lambda Q^T built on the device as bench.py does (n = 16384),
+exact pairs (Lambda, Q). Gates: converged, eigenvalue count, eigenvalues to
+1e-10 of max(|lambda|), subspace sine to max(1e-8, Davis-Kahan bound)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _laplacian_basis(m, lo, hi):
+    h = 1.0 / (m + 1)
+    p = np.arange(1, m + 1)
+    lam, cols = [], []
+    for j in range(1, m + 1):
+        for k in range(1, m + 1):
+            v = (4.0 / h ** 2) * (math.sin(j * math.pi * h / 2) ** 2 + math.sin(k * math.pi * h / 2) ** 2)
+            if lo < v < hi:
+                u = np.sin(j * math.pi * h * p)[None, :] * np.sin(k * math.pi * h * p)[:, None]
+                cols.append(u.ravel() / np.linalg.norm(u))
+                lam.append(v)
+    order = np.argsort(lam)
+    return np.asarray(lam)[order], np.stack(cols, axis=1)[:, order]
+
+
+def test_cfg3_laplacian_exact():
+    import paper_1605_08771_b200 as P
+    from paper_1605_08771_b200 import configs as CF
+    c = CF.resolved(3, CF.laplacian_eigenvalues(96))
+    A = CF.laplacian_2d()
+    lam, U = _laplacian_basis(96, c["lo"], c["hi"])
+    assert len(lam) == 200
+    sol = P.feast_solve(A, P.SearchInterval(c["lo"], c["hi"]),
+                        P.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"]))
+    assert sol.converged and len(sol.eigenvalues) == 200
+    scale = 4.0 * 97 ** 2 * 2
+    assert np.abs(np.sort(sol.eigenvalues) - lam).max() <= 1e-10 * scale
+    V = sol.eigenvectors
+    sine = np.linalg.norm(V - U @ (U.T @ V), 2)
+    R = np.linalg.norm(A @ V - V * sol.eigenvalues)
+    allv = CF.laplacian_eigenvalues(96)
+    outside = allv[(allv <= c["lo"]) | (allv >= c["hi"])]
+    gap = np.abs(sol.eigenvalues[:, None] - outside[None, :]).min()
+    assert sine <= max(1e-8, R / gap), (sine, R, gap)
+
+
+def test_cfg4_exact():
+    import torch
+    import paper_1605_08771_b200 as P
+    from paper_1605_08771_b200 import configs as CF
+    vals = CF.spectrum(4, P.uniform_values)
+    c = CF.resolved(4, vals)
+    n = c["n"]
+    G = torch.from_numpy(P.gaussian_block(n, n, 1004)).cuda()
+    Q, _ = torch.linalg.qr(G)
+    del G
+    inside = (vals > c["lo"]) & (vals < c["hi"])
+    A = (Q * torch.from_numpy(vals).cuda()) @ Q.T
+    A = 0.5 * (A + A.T)
+    Ah = A.cpu().numpy()  # symmetric: row-major storage == column-major
+    del A
+    torch.cuda.empty_cache()
+    sol = P.feast_solve(np.asfortranarray(Ah.T), P.SearchInterval(c["lo"], c["hi"]),
+                        P.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"]))
+    assert sol.converged and len(sol.eigenvalues) == int(inside.sum())
+    assert np.abs(np.sort(sol.eigenvalues) - vals[inside]).max() <= 1e-10 * np.abs(vals).max()
+    V = torch.from_numpy(np.ascontiguousarray(sol.eigenvectors)).cuda()
+    Qi = Q[:, torch.from_numpy(np.nonzero(inside)[0]).cuda()]
+    sine = torch.linalg.matrix_norm(V - Qi @ (Qi.T @ V), ord=2).item()
+    gap = np.abs(sol.eigenvalues[:, None] - vals[~inside][None, :]).min()
+    R = max(sol.residual_norms) * np.sqrt(len(sol.eigenvalues))
+    assert sine <= max(1e-8, R / gap), (sine, R, gap)

@@ -1,7 +1,7 @@
 """Generate tests/golden/oracle_cfg<k>.json: the CPU oracle's FEAST / XFEAST /
 RFEAST results (traces, iteration/converged counts, eigenvalues) on a BASELINE
 configuration, so the GPU parity tests need not rerun minutes of CPU work.
-Usage: python tools/gen_golden.py <cfg> [threads]   (run in the build container)"""
+Usage: python tools/gen_golden.py <cfg> [threads] [drivers,...]   (run in the build container)"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle as O
@@ -15,7 +15,8 @@ c = CF.resolved(idx, vals)
 A = CF.laplacian_2d() if idx == 3 else O.assemble_matrix(vals, O.seeded_orthogonal(len(vals), 1000 + idx))
 out = {"cfg": idx, "config": c, "oracle_threads": O.get_threads(), "generator": "tools/gen_golden.py",
        "drivers": {}}
-for d in ("feast_solve", "xfeast_solve", "rfeast_solve"):
+drivers = sys.argv[3].split(",") if len(sys.argv) > 3 else ["feast_solve", "xfeast_solve", "rfeast_solve"]
+for d in drivers:
     t = time.time()
     s = getattr(O, d)(A, O.SearchInterval(c["lo"], c["hi"]),
                       O.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"], s=c["s"]))
