@@ -109,6 +109,8 @@ int fl_debug_zgemm(fl_ctx* ctx, int M, int N, int K, int batch, int iters, doubl
                    fl_err* err);
 /* cycle counts of the LU panel kernel's phases (instrumentation) */
 int fl_debug_panel_profile(double* out8, int reset);
+/* per-warp clock64 trace of the first on-chip panel (builds with FL_PANEL_TRACE) */
+int fl_debug_panel_trace(long long* out, int max);
 int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long long* launches,
                    fl_err* err);
 

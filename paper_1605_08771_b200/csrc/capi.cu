@@ -1161,6 +1161,8 @@ int fl_debug_panel_profile(double* out8, int reset) {
     return FL_OK;
 }
 
+int fl_debug_panel_trace(long long* out, int max) { return fl::res_panel_trace(out, max); }
+
 int fl_ctx_set_streams(fl_ctx* ctx, int n) {
     CtxLock lk(ctx);
     ctx->nstreams = std::max(1, std::min(n, (int)ctx->aux.size()));

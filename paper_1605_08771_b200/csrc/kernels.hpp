@@ -58,6 +58,8 @@ void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int
                   cudaStream_t s);
 // Cycle counts of the panel kernel phases (node 0, rank 0, thread 0).
 void panel_profile(double* out8, bool reset);
+// clock64 trace of the on-chip panel (FL_PANEL_TRACE builds)
+int res_panel_trace(long long* out, int max);
 // Apply a panel's 64 row interchanges (ptab) to the columns [a0,a1) U [b0,b1).
 void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int batch,
                   cudaStream_t s);

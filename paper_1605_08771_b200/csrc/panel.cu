@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -101,7 +102,14 @@ __device__ int net_permutation(SH& sh, int first, const int* piv, int count, int
 
 __device__ unsigned long long g_panel_prof[8];
 
+void res_panel_profile(double* out8, bool reset);
+
 void panel_profile(double* out8, bool reset) {
+    const char* e = std::getenv("FEASTLAB_PANEL");
+    if (!(e && std::strcmp(e, "reg") == 0)) {
+        res_panel_profile(out8, reset);
+        return;
+    }
     unsigned long long h[8];
     cudaMemcpyFromSymbol(h, g_panel_prof, sizeof(h));
     for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
@@ -495,8 +503,18 @@ static void launch_panel_cl(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatc
         launch_reg<2, 8, 512, CL>(F, N, k0, ipiv, ptab, Inv, batch, s);
 }
 
+bool launch_panel_resident(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
+                           cudaStream_t s);
+
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
                   cudaStream_t s) {
+    // panels of <= 4096 rows: the on-chip panel (panel_res.cu) unless
+    // FEASTLAB_PANEL=reg selects the register-leaf kernel below everywhere
+    static const bool resident = [] {
+        const char* e = std::getenv("FEASTLAB_PANEL");
+        return !(e && std::strcmp(e, "reg") == 0);
+    }();
+    if (resident && launch_panel_resident(F, N, k0, ipiv, ptab, Inv, batch, s)) return;
     // 4-CTA clusters for short panels of small problems (<= 2048 rows of an
     // N <= 4096 matrix: 2 rows per thread, half the SMs a panel holds beside
     // the GEMMs); 8-CTA clusters otherwise. Measured (ms per application):

@@ -27,7 +27,9 @@ rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.2), 1)
 f = P.FilterApplier(A, rule, ctx=ctx)
 f.apply(X)
 _lib.lib().fl_debug_panel_profile(out, 1)
-names = ["cand+publish", "cluster.sync", "pivot fetch", "update", "leaf store+sync", "perm+sync", "trsm", "inner update"]
+import os
+names = (["cand+publish", "cluster.sync", "pivot fetch", "update", "leaf store+sync", "perm+sync", "trsm", "inner update"]
+         if os.environ.get("FEASTLAB_PANEL") == "reg" else
+         ["load/store/Linv", "cand", "BAR+CTAred", "push", "deferred", "mbar wait", "red+update", "transitions"])
 tot = sum(out)
-print("panel phases (cycles, 1 node, all panels):", {k: int(v) for k, v in zip(names, out)}, "total", int(tot),
-      "-> us per column", tot / 1.965e3 / n)
+print("panel phases per column (cycles, mean over the 8 warps of rank 0, node 0):", {k: int(v / 8 / n) for k, v in zip(names, out)}, "total", int(tot / 8 / n))
