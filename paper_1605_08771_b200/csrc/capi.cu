@@ -182,6 +182,7 @@ struct fl_filter {
     DBuf fac_re, fac_im, ipiv, perm, bad, ptab;
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     int fac_slots = 0;
+    int panel_res_rows = 4096;   // see panel_res_rows()
     std::vector<char> factored;  // cache mode, per local node
     DBuf w_re, w_im;             // W for all local nodes (N x P each)
     long w_stride = 0;
@@ -371,7 +372,7 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     }();
     auto panel = [&](int k, int* tab) {
         Prof pr(ctx, P_PANEL, 0.0, 1, sp);  // also writes L_kk^{-1} into Inv
-        if (!(dbg_skip & 1)) launch_panel(F, N, k, ipiv, tab, Inv, G, sp);
+        if (!(dbg_skip & 1)) launch_panel(F, N, k, ipiv, tab, Inv, G, sp, f->panel_res_rows);
     };
     auto swaps = [&](const int* tab, int a0, int a1, int b0, int b1, cudaStream_t s) {
         if (dbg_skip & 4) return;
@@ -487,6 +488,23 @@ bool graphs_enabled() {
     return on;
 }
 
+// Few local nodes (latency-bound: the per-node LU chain sets the step time,
+// e.g. 2 nodes per GPU at 8 GPUs) -> the on-chip panel for every panel of
+// <= 4096 rows; many local nodes (throughput-bound: panels overlap other
+// chunks' GEMMs) -> the on-chip panel only below FEASTLAB_PANEL_RES_ROWS rows
+// (default 2048), so tall panels keep co-residing with GEMM CTAs.
+int panel_res_rows(int local_nodes) {
+    static const int thr = [] {
+        const char* e = std::getenv("FEASTLAB_PANEL_RES_ROWS");
+        return e ? std::atoi(e) : 2048;
+    }();
+    static const int few = [] {
+        const char* e = std::getenv("FEASTLAB_PANEL_FEW_NODES");
+        return e ? std::atoi(e) : 4;
+    }();
+    return local_nodes <= few ? 4096 : thr;
+}
+
 size_t free_bytes() {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -536,6 +554,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // Node chunks run concurrently on the context's auxiliary streams so one
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
     const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
+    f->panel_res_rows = panel_res_rows(L);
     long long new_facts = 0;
     // everything below is stream work only (no host synchronisation), so a
     // non-cache application is one CUDA graph: ~2.8k launches on 9 streams

@@ -54,8 +54,11 @@ void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& 
 // Factor panel columns [k0, k0+64) of every node (cluster kernel). ipiv[b*N + j];
 // ptab[b*257 ...] receives the panel's net row permutation (count, rows, sources);
 // Inv block k0/64 (see launch_trinv) receives L_kk^{-1}.
+// Panels of at most `res_rows` rows (<= 4096) use the on-chip cluster panel
+// (panel_res.cu, latency-optimised, whole SMs); taller ones the register-leaf
+// panel that co-resides with the GEMM CTAs (throughput-optimised).
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
-                  cudaStream_t s);
+                  cudaStream_t s, int res_rows = 4096);
 // Cycle counts of the panel kernel phases (node 0, rank 0, thread 0).
 void panel_profile(double* out8, bool reset);
 // clock64 trace of the on-chip panel (FL_PANEL_TRACE builds)

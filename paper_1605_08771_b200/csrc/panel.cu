@@ -507,14 +507,16 @@ bool launch_panel_resident(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch
                            cudaStream_t s);
 
 void launch_panel(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv, int batch,
-                  cudaStream_t s) {
-    // panels of <= 4096 rows: the on-chip panel (panel_res.cu) unless
+                  cudaStream_t s, int res_rows) {
+    // panels of <= res_rows rows: the on-chip panel (panel_res.cu) unless
     // FEASTLAB_PANEL=reg selects the register-leaf kernel below everywhere
     static const bool resident = [] {
         const char* e = std::getenv("FEASTLAB_PANEL");
         return !(e && std::strcmp(e, "reg") == 0);
     }();
-    if (resident && launch_panel_resident(F, N, k0, ipiv, ptab, Inv, batch, s)) return;
+    if (resident && N - k0 <= res_rows &&
+        launch_panel_resident(F, N, k0, ipiv, ptab, Inv, batch, s))
+        return;
     // 4-CTA clusters for short panels of small problems (<= 2048 rows of an
     // N <= 4096 matrix: 2 rows per thread, half the SMs a panel holds beside
     // the GEMMs); 8-CTA clusters otherwise. Measured (ms per application):
