@@ -57,6 +57,7 @@ _SIGS = {
     "fl_ctx_set_profiling": (_I, [_P, _I]),
     "fl_ctx_set_streams": (_I, [_P, _I]),
     "fl_debug_panel_profile": (_I, [_P, _I]),
+    "fl_debug_panel_trace": (_I, [_P, _I]),
     "fl_ctx_profile_dump": (_I, [_P, _P, _I]),
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
     "fl_zgemm_mode": (_I, [_I]),
