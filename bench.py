@@ -7,7 +7,10 @@ ascending-node weighted accumulation (+ NCCL all-reduce across ranks when the
 nodes are sharded). value = filter FP64 GFLOP/s of the whole job,
 F_filter = n_c (8/3 n^3 + 8 n^2 m0) per step.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl b200|reference]
+
+Default workload: cfg4 (n = 16384, m0 = 512, n_c = 32), the configuration
+BASELINE.json names for the 1/2/4/8-GPU strong-scaling run; it fits one B200.
 
 Under torchrun (N > 1) each rank owns n_c/N contiguous nodes; timing is the
 max over ranks of CUDA-event time on the library stream. --impl reference
@@ -34,19 +37,27 @@ METRIC = "FEAST time-to-solution and filter-solve FP64 GFLOP/s vs FP64 peak, 1/2
 # FP64 DMMA peak measured on this pool's B200 by tools/fp64_peak.cu (profiles/fp64_peak.json);
 # MEASURED_PEAKS.json carries no FP64 entry.
 FP64_DMMA_PEAK_TFLOPS = 37.08
+# CPU samples are one contour node; above this order (cfg4) the node is taken
+# at this order so a sample stays ~10 s of host work (the rate, GFLOP/s, is
+# what is reported)
+CPU_SAMPLE_MAX_N = 8192
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 3 for n >= 16384, else 5)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=8, help="node chunks in flight (1..8)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 3 if a.config == 4 else 5
+    return a
 
 
 def filter_flops(n, p, nc):
@@ -169,7 +180,7 @@ def cpu_sample(c, threads):
     from paper_1605_08771_b200 import configs as CF  # noqa: F401
 
     O.set_threads(threads)
-    n, p = c["n"], c["m0"]
+    n, p = min(c["n"], CPU_SAMPLE_MAX_N), c["m0"]
     rng = np.random.default_rng(0)
     M = rng.standard_normal((n, n))
     A = np.asfortranarray(0.5 * (M + M.T) / np.sqrt(n))
@@ -180,7 +191,7 @@ def cpu_sample(c, threads):
     O.apply_filter(A, one, X)
     dt = time.perf_counter() - t0
     flops = filter_flops(n, p, 1)
-    return flops / dt / 1e9, dt
+    return flops / dt / 1e9, dt, n
 
 
 # ------------------------------------------------------------------ reference arm
@@ -199,7 +210,7 @@ def run_reference(args, rank, world):
     rates = []
     t_all = 0.0
     for _ in range(args.steps):
-        r, dt = cpu_sample(c, threads)
+        r, dt, ns = cpu_sample(c, threads)
         rates.append(r)
         t_all += dt
     value = float(np.mean(rates))
@@ -212,10 +223,10 @@ def run_reference(args, rank, world):
                    "n_c": c["n_c"]},
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
                          "kind": "port",
-                         "sample": "one contour node per step (zI-A LU + m0-RHS solve + "
-                                   "accumulate) of the workload, oracle restatement of "
-                                   "proj/src/filterop.cpp on OpenBLAS; reference (Eigen) "
-                                   "unbuildable here"},
+                         "sample": f"one contour node per step (zI-A LU + m0-RHS solve + "
+                                   f"accumulate) of the workload at n={ns}, m0={c['m0']}, "
+                                   "oracle restatement of proj/src/filterop.cpp on OpenBLAS; "
+                                   "reference (Eigen) unbuildable here"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -284,10 +295,12 @@ def run_b200(args, rank, world, local_rank):
     clk = clocks.stop()
     # per-kernel-class CUDA events over K more steps with the node chunks
     # serialised (1 stream), so each class's event time is its own
+    # (one step for the 16384 workload: a step is seconds long)
+    prof_steps = 1 if n >= 16384 else args.steps
     ctx.set_streams(1)
     ctx.set_profiling(True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(prof_steps):
         step()
     e1.record(stream)
     e1.synchronize()
@@ -308,19 +321,29 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    e2e_steps = min(args.steps, 2) if n >= 16384 else args.steps
     e0.record(stream)  # H2D of X and D2H of Y run on the library stream
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         filt.apply(Xh, acc, out=Yh)
     e1.record(stream)
     e1.synchronize()
     e2e_s = e0.elapsed_time(e1) * 1e-3
     if dist:
         e2e_s = D.max_over_ranks(e2e_s)
-    e2e_value = total_flops / e2e_s / 1e9
+    e2e_value = filter_flops(n, p, nc) * e2e_steps / e2e_s / 1e9
+    # the filter's factor slots (up to 16 LUs) must not coexist with the
+    # cached solve's n_c / N factors below
+    del filt
+    gc.collect()
+    torch.cuda.empty_cache()
 
     # time-to-solution: full feast_solve (host A in, Solution out) once
+    # Under torchrun every rank runs the same driver on the multi-rank
+    # context: its filter factors the rank's contour nodes and all-reduces the
+    # sum (NCCL); the Rayleigh-Ritz tail runs redundantly (bitwise identical
+    # on every rank). TTS = max over ranks of the driver call's wall time.
     tts = None
-    if not args.no_tts and rank == 0 and world == 1:
+    if not args.no_tts:
         Ah = None
         try:
             A2, _, _ = build_workload(args.config, local_rank)
@@ -332,9 +355,14 @@ def run_b200(args, rank, world, local_rank):
             for cache in (False, True):  # report the cache off and on
                 cfg = P.SolverConfig(m0=p, n_c=nc, tol=c["tol"], max_iter=c["max_iter"],
                                      cache_factorizations=cache)
+                if dist:
+                    dist.barrier()
                 t0 = time.perf_counter()
                 sol = P.feast_solve(S, P.SearchInterval(c["lo"], c["hi"]), cfg, ctx=ctx)
-                rec = {"seconds": round(time.perf_counter() - t0, 4),
+                dt = time.perf_counter() - t0
+                if dist:
+                    dt = D.max_over_ranks(dt)
+                rec = {"seconds": round(dt, 4),
                        "iterations": sol.iterations, "converged": sol.converged,
                        "eigenpairs": len(sol.eigenvalues), "expected_inside": c["inside"],
                        "max_residual": sol.trace[-1].max_residual if sol.trace else None,
@@ -369,9 +397,9 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_cpu_baseline and world == 1:
         try:
             threads = os.cpu_count() or 1
-            rate, dt = cpu_sample(c, threads)
+            rate, dt, ns = cpu_sample(c, threads)
             cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                   "sample": f"one contour node (n={n}, m0={p}) of the workload: LU + solve + "
+                   "sample": f"one contour node (n={ns}, m0={p}) of the workload: LU + solve + "
                              f"accumulate in {dt:.2f} s, oracle restatement on OpenBLAS"}
         except Exception as e:
             cpu = {"error": f"{type(e).__name__}: {e}"}
@@ -400,12 +428,12 @@ def run_b200(args, rank, world, local_rank):
                      "peak_source": "measured FP64 DMMA burst, tools/fp64_peak.cu "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
                      "share_of_step": round(zms / ms_serial, 4) if ms_serial else None,
-                     "launches_per_step": zl / args.steps,
-                     "timing": "CUDA events per launch, node chunks serialised (1 stream) "
-                               "over K extra steps"},
-        "serial_ms_per_step": round(ms_serial / args.steps, 3),
-        "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 3),
-                        "work_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
+                     "launches_per_step": zl / prof_steps,
+                     "timing": f"CUDA events per launch, node chunks serialised (1 stream) "
+                               f"over {prof_steps} extra step(s)"},
+        "serial_ms_per_step": round(ms_serial / prof_steps, 3),
+        "kernels": {k: {"ms_per_step": round(v[0] / prof_steps, 3),
+                        "work_per_step": v[1] / prof_steps, "launches_per_step": v[2] / prof_steps}
                     for k, v in prof.items()},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * n * p, "d2h_bytes_per_step": 8 * n * p},
