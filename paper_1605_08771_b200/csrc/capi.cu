@@ -31,6 +31,7 @@ namespace {
 using namespace fl;
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int FL_MAX_BLOCK_PANELS = 4;
 
 struct Fail {
     int code;
@@ -183,6 +184,8 @@ struct fl_filter {
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     int fac_slots = 0;
     int panel_res_rows = 4096;   // see panel_res_rows()
+    int lu_panels = 2;           // LU outer block = lu_panels x 64 columns (block_panels())
+    int solve_panels = 4;        // triangular-solve row block = solve_panels x 64 rows
     std::vector<char> factored;  // cache mode, per local node
     DBuf w_re, w_im;             // W for all local nodes (N x P each)
     long w_stride = 0;
@@ -364,8 +367,11 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         Prof pr(ctx, P_TRSM, 8.0 * T * T * nc * G, 1, s);
         launch_zgemm_set(u, G, s);
     };
-    // two pivot tables: panel B's must not overwrite panel A's before st uses it
-    int* tabs[2] = {ptab, f->ptab.i() + (long)(f->fac_slots + s0) * (4 * T + 1)};
+    // one pivot table per panel of an outer block: panel j+1's must not
+    // overwrite panel j's before st has applied it
+    const int NPB = f->lu_panels;  // panels per outer block (2: 128 columns, 4: 256)
+    int* tabs[FL_MAX_BLOCK_PANELS];
+    for (int j = 0; j < NPB; ++j) tabs[j] = ptab + (long)(j * f->fac_slots) * (4 * T + 1);
     static const int dbg_skip = [] {  // timing experiments only: results are wrong
         const char* e = std::getenv("FEASTLAB_DEBUG_SKIP");
         return e ? std::atoi(e) : 0;
@@ -379,44 +385,61 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         Prof pr(ctx, P_LASWP, 0.0, 1, s);
         launch_laswp(F, a0, a1, b0, b1, tab, G, s);
     };
-    // Outer blocks of 128 columns = panels A (kA) and B (kB = kA + 64). The
-    // panel stream factors BOTH panels while the main stream finishes the
-    // previous block's trailing update (look-ahead); the trailing update then
-    // has K = 128 (half the C-tile traffic of K = 64):
-    //   sp: panel A | A-swaps on B's columns | U_A[:, B] = L_AA^-1 (.) |
-    //       A[kB:, B] -= L_A U_A[:, B] | panel B                       -> ev_panel
-    //   st: A-swaps, B-swaps on the other columns | U_A[:, rest] |
-    //       A[kB, rest] -= L_A[kB,:] U_A[:, rest] | U_B = L_BB^-1 (.) |
-    //       A[kB+64:, rest] -= [L_A L_B] [U_A; U_B]  (next block's 128 columns
-    //       first -> ev_next, then the remainder)
+    // Outer blocks of NPB panels (BW = 64 NPB columns), panels k_j = k0 + 64 j.
+    // The panel stream factors all of a block's panels while the main stream
+    // finishes the previous block's trailing update (look-ahead); the trailing
+    // update then has K = BW (C-tile traffic and GEMM fill/drain per flop fall
+    // as 1/BW):
+    //   sp: for j: [ panel j-1's swaps on the block's columns left of it |
+    //               panels 0..j-1's swaps on panel j's columns |
+    //               U rows k_0..k_j of panel j's columns (L_ii^-1 and in-block
+    //               updates) | A[k_j:, panel j] -= L[k_j:, k_0:k_j] U ] panel j
+    //                                                                -> ev_panel
+    //   st: every panel's swaps on the other columns | the block's U rows of
+    //       the columns right of it (L_jj^-1, in-block updates) |
+    //       A[c0:, c0:] -= L[c0:, block] U[block, c0:]  (the next block's BW
+    //       columns first -> ev_next, then the remainder)
     CK(cudaEventRecord(ev_next, st));  // shift done: block 0 may start
-    for (int kA = 0; kA < N; kA += 2 * T) {
-        const int kB = kA + T, c0 = kB + T;
+    for (int k0 = 0; k0 < N; k0 += NPB * T) {
+        const int np = std::min(NPB, (N - k0) / T);
+        const int c0 = k0 + np * T;
         CK(cudaStreamWaitEvent(sp, ev_next, 0));
-        panel(kA, tabs[0]);
-        if (kB < N) {
-            swaps(tabs[0], kB, kB + T, 0, 0, sp);
-            linv(kA, kB, T, sp);
-            sub(N - kB, T, T, kB, kA, kA, kB, kB, kB, sp);
-            panel(kB, tabs[1]);
+        for (int j = 0; j < np; ++j) {
+            const int kj = k0 + j * T;
+            if (j > 0) {
+                // the block's earlier L columns must carry panel j-1's
+                // interchanges before they update panel j (the last panel's
+                // reach them on st, off the look-ahead chain)
+                if (j >= 2) swaps(tabs[j - 1], k0, kj - T, 0, 0, sp);
+                for (int i = 0; i < j; ++i) swaps(tabs[i], kj, kj + T, 0, 0, sp);
+                for (int i = 0; i < j; ++i) {
+                    const int ki = k0 + i * T;
+                    linv(ki, kj, T, sp);
+                    if (i + 1 < j) sub((j - 1 - i) * T, T, T, ki + T, ki, ki, kj, ki + T, kj, sp);
+                }
+                sub(N - kj, T, j * T, kj, k0, k0, kj, kj, kj, sp);
+            }
+            panel(kj, tabs[j]);
         }
         CK(cudaEventRecord(ev_panel, sp));
         CK(cudaStreamWaitEvent(st, ev_panel, 0));
-        if (kB >= N) {
-            swaps(tabs[0], 0, kA, 0, 0, st);
-            break;
-        }
-        swaps(tabs[0], 0, kA, c0, N, st);
-        swaps(tabs[1], 0, kB, c0, N, st);
         const int rest = N - c0;
+        for (int j = 0; j < np; ++j) {
+            // panels 1..np-2 already swapped the block's columns left of them (sp)
+            const int left = j == np - 1 ? k0 + j * T : k0;
+            if (rest > 0) swaps(tabs[j], 0, left, c0, N, st);
+            else swaps(tabs[j], 0, left, 0, 0, st);
+        }
         if (rest <= 0) break;
-        linv(kA, c0, rest, st);
-        sub(T, rest, T, kB, kA, kA, c0, kB, c0, st);
-        linv(kB, c0, rest, st);
-        const int nxt = std::min(2 * T, rest);
-        sub(rest, nxt, 2 * T, c0, kA, kA, c0, c0, c0, st);
+        for (int j = 0; j < np; ++j) {
+            const int kj = k0 + j * T;
+            linv(kj, c0, rest, st);
+            if (j + 1 < np) sub((np - 1 - j) * T, rest, T, kj + T, kj, kj, c0, kj + T, c0, st);
+        }
+        const int nxt = std::min(np * T, rest);
+        sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st);
         CK(cudaEventRecord(ev_next, st));
-        sub(rest, rest - nxt, 2 * T, c0, kA, kA, c0 + nxt, c0, c0 + nxt, st);
+        sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st);
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
@@ -455,27 +478,31 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
         Prof pr(ctx, P_ZGEMM, 8.0 * M * P * K * G, 1, st);
         launch_zgemm_sub(g, G, st);
     };
-    // 128-row steps, so the long updates have K = 128 (cf. the LU):
-    // forward (unit lower): W_i = L_ii^-1 W_i; W_{i+1} -= L_{i+1,i} W_i;
-    //   W_{i+1} = L^-1 W_{i+1}; W_{i+2:} -= L_{i+2:, i:i+2} W_{i:i+2}
+    // row blocks of NPB tiles (cf. the LU), so the long updates have K = 64 NPB:
+    // forward (unit lower), block [r0, r0 + np 64): W_j = L_jj^-1 W_j and the
+    //   in-block updates below it, then W[r0 + np 64:] -= L[.., block] W_block
     const int T = FL_TILE;
-    for (int ib = 0; ib < NB; ib += 2) {
-        const int r0 = ib * T;
-        tri(ib, r0);
-        if (ib + 1 >= NB) break;
-        sub(T, T, r0 + T, r0, r0, r0 + T);
-        tri(ib + 1, r0 + T);
-        sub(N - r0 - 2 * T, 2 * T, r0 + 2 * T, r0, r0, r0 + 2 * T);
+    const int NPB = f->solve_panels;
+    for (int ib = 0; ib < NB; ib += NPB) {
+        const int np = std::min(NPB, NB - ib), r0 = ib * T;
+        for (int j = 0; j < np; ++j) {
+            const int rj = r0 + j * T;
+            tri(ib + j, rj);
+            if (j + 1 < np) sub((np - 1 - j) * T, T, rj + T, rj, rj, rj + T);
+        }
+        sub(N - r0 - np * T, np * T, r0 + np * T, r0, r0, r0 + np * T);
     }
-    // backward (upper), from the bottom in 128-row steps aligned to the end
-    for (int ib = NB - 1; ib >= 0; ib -= 2) {
-        const int r1 = ib * T;  // lower block of the pair
-        tri(NB + ib, r1);
-        if (ib == 0) break;
-        const int r0 = r1 - T;
-        sub(T, T, r0, r1, r1, r0);
-        tri(NB + ib - 1, r0);
-        sub(r0, 2 * T, 0, r0, r0, 0);
+    // backward (upper), blocks aligned to the end: within a block from its
+    // last tile up (W_j = U_jj^-1 W_j, then the in-block rows above it), then
+    // W[:r0] -= U[:r0, block] W_block
+    for (int ie = NB; ie > 0; ie -= NPB) {
+        const int np = std::min(NPB, ie), ib = ie - np, r0 = ib * T;
+        for (int j = np - 1; j >= 0; --j) {
+            const int rj = r0 + j * T;
+            tri(NB + ib + j, rj);
+            if (j > 0) sub(j * T, T, r0, rj, rj, r0);
+        }
+        sub(r0, np * T, 0, r0, r0, 0);
     }
 }
 
@@ -503,6 +530,16 @@ int panel_res_rows(int local_nodes) {
         return e ? std::atoi(e) : 4;
     }();
     return local_nodes <= few ? 4096 : thr;
+}
+
+// Panels per LU outer block / tiles per triangular-solve row block (1..4).
+// Many local nodes (throughput-bound): 4, so the trailing updates run with
+// K = 256; few (latency-bound: the per-node panel chain sets the step time):
+// 2, so the look-ahead stream has half as many panels to factor per block.
+int block_panels(const char* env, int dflt) {
+    const char* e = std::getenv(env);
+    const int v = e ? std::atoi(e) : dflt;
+    return std::max(1, std::min(FL_MAX_BLOCK_PANELS, v));
 }
 
 size_t free_bytes() {
@@ -543,7 +580,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->fac_im.ensure(sizeof(double) * (size_t)fstride * slots);
         f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
         f->perm.ensure(sizeof(int) * (size_t)N * slots);
-        f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * 2 * slots);
+        f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * FL_MAX_BLOCK_PANELS * slots);
         f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->fac_slots = slots;
@@ -555,6 +592,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
     const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
     f->panel_res_rows = panel_res_rows(L);
+    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? 4 : 2);
+    f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4);
     long long new_facts = 0;
     // everything below is stream work only (no host synchronisation), so a
     // non-cache application is one CUDA graph: ~2.8k launches on 9 streams
