@@ -41,7 +41,9 @@ enum fl_status {
   FL_SINGULAR_NODE = 4,    /* runtime_error of filterop.cpp:19-22: index, z          */
   FL_CUDA = 5,
   FL_NCCL = 6,
-  FL_OOM = 7
+  FL_OOM = 7,
+  FL_MATRIX_MARKET = 8,    /* feastlab::MatrixMarketError (matrix_market.hpp:9-16): index = line */
+  FL_NOT_SYMMETRIC = 9     /* feastlab::NotSymmetricError (matrix_market.hpp:18-21): index = line */
 };
 
 enum fl_loc { FL_HOST = 0, FL_DEVICE = 1 };
@@ -227,6 +229,13 @@ int fl_make_initial_guess(fl_ctx* ctx, int n, int m0, uint64_t seed, double* X, 
 /* select_pairs ordering (ritz.cpp:124-151): chosen[0..*nchosen-1] */
 int fl_select_pairs(const double* vals, const double* norms, const unsigned char* inside, int p,
                     int m0, double lo, double hi, int* chosen, int* nchosen, fl_err* err);
+/* read_matrix_market (matrix_market.cpp:31-117) into a column-major host
+   buffer: A == NULL queries *n only (banner + size line). Errors: FL_NOT_SYMMETRIC /
+   FL_MATRIX_MARKET with err->index = the 1-based line; FL_RUNTIME_ERROR when the
+   file cannot be opened. Pass the result to fl_matrix_create for the upload. */
+int fl_mm_read(const char* path, int* n, double* A, int lda, fl_err* err);
+/* write_matrix_market (matrix_market.cpp:119-147); format 0 = coordinate, 1 = array */
+int fl_mm_write(const char* path, const double* A, int n, int lda, int format, fl_err* err);
 /* seeded column-major N(0,1) / U[lo,hi) fills (fixture generation) */
 void fl_gaussian_fill(double* out, long long count, uint64_t seed);
 void fl_uniform_fill(double* out, long long count, double lo, double hi, uint64_t seed);

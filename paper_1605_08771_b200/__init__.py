@@ -8,6 +8,7 @@ kernels behind the C ABI of include/feastlab_b200.h plus the drop-in C++ layer
 from . import _lib  # noqa: F401
 from .feastlab import *  # noqa: F401,F403
 from .feastlab import (CholeskyError, Context, FeastCudaError, FeastRuntimeError,  # noqa: F401
-                       InvalidArgument, SingularNodeError)
+                       InvalidArgument, MatrixMarketError, NotSymmetricError,
+                       SingularNodeError)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FEASTLAB_LIB") or os.path.join(HERE, "lib", "libfeastlab_b200.so")
 
 FL_OK, FL_INVALID_ARGUMENT, FL_RUNTIME_ERROR, FL_CHOLESKY, FL_SINGULAR_NODE, FL_CUDA, FL_NCCL, \
-    FL_OOM = range(8)
+    FL_OOM, FL_MATRIX_MARKET, FL_NOT_SYMMETRIC = range(10)
 FL_HOST, FL_DEVICE = 0, 1
 FL_REDUCE_SUM, FL_REDUCE_ORDERED = 0, 1
 
@@ -58,6 +58,8 @@ _SIGS = {
     "fl_ctx_set_streams": (_I, [_P, _I]),
     "fl_debug_panel_profile": (_I, [_P, _I]),
     "fl_debug_panel_trace": (_I, [_P, _I]),
+    "fl_mm_read": (_I, [C.c_char_p, _P, _P, _I, _P]),
+    "fl_mm_write": (_I, [C.c_char_p, _P, _I, _I, _I, _P]),
     "fl_ctx_profile_dump": (_I, [_P, _P, _I]),
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
     "fl_zgemm_mode": (_I, [_I]),

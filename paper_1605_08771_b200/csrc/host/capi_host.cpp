@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "feastlab/drivers.hpp"
+#include "feastlab/matrix_market.hpp"
 #include "feastlab_b200.h"
 
 namespace feastlab {
@@ -34,6 +35,12 @@ int guarded(fl_err* err, F&& body) {
     try {
         body();
         return FL_OK;
+    } catch (const NotSymmetricError& x) {
+        if (err) err->index = x.line;
+        return fail(err, FL_NOT_SYMMETRIC, x.what());
+    } catch (const MatrixMarketError& x) {
+        if (err) err->index = x.line;
+        return fail(err, FL_MATRIX_MARKET, x.what());
     } catch (const CholeskyError& x) {
         if (err) {
             err->pivot = x.pivot;
@@ -152,6 +159,22 @@ int fl_symmetric_matrix(const double* M, int n, int ldm, double sym_tol, double*
             throw std::invalid_argument("SymmetricMatrix: matrix must be square, n >= 1");
         SymmetricMatrix S(M, n, ldm, sym_tol);
         std::memcpy(out, S.mat().data(), sizeof(double) * (size_t)n * n);
+    });
+}
+
+int fl_mm_read(const char* path, int* n, double* A, int lda, fl_err* err) {
+    return guarded(err, [&] {
+        if (!path) throw std::invalid_argument("read_matrix_market: null path");
+        const int m = read_matrix_market_into(path, A, lda);
+        if (n) *n = m;
+    });
+}
+
+int fl_mm_write(const char* path, const double* A, int n, int lda, int format, fl_err* err) {
+    return guarded(err, [&] {
+        if (!path || n < 1 || lda < n) throw std::invalid_argument("write_matrix_market: bad arguments");
+        write_matrix_market(A, n, lda, path,
+                            format ? MatrixMarketFormat::array : MatrixMarketFormat::coordinate);
     });
 }
 

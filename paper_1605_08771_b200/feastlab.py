@@ -9,6 +9,7 @@ libfeastlab_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -44,6 +45,18 @@ class SingularNodeError(FeastRuntimeError):
         self.z = z
 
 
+class MatrixMarketError(FeastRuntimeError):
+    """feastlab::MatrixMarketError (proj/include/feastlab/matrix_market.hpp:9-16)"""
+
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
+class NotSymmetricError(MatrixMarketError):
+    """feastlab::NotSymmetricError (proj/include/feastlab/matrix_market.hpp:18-21)"""
+
+
 class FeastCudaError(RuntimeError):
     """CUDA / NCCL / device-memory failure (no CPU fallback exists)."""
 
@@ -58,6 +71,10 @@ def _check(code, err):
         raise CholeskyError(msg, err.pivot, err.index)
     if code == L.FL_SINGULAR_NODE:
         raise SingularNodeError(msg, err.index, complex(err.z_re, err.z_im))
+    if code == L.FL_NOT_SYMMETRIC:
+        raise NotSymmetricError(msg, err.index)
+    if code == L.FL_MATRIX_MARKET:
+        raise MatrixMarketError(msg, err.index)
     if code == L.FL_RUNTIME_ERROR:
         raise FeastRuntimeError(msg)
     raise FeastCudaError(f"[status {code}] {msg}")
@@ -266,6 +283,26 @@ class SymmetricMatrix:
 
     def mat(self):
         return self._mat
+
+
+def read_matrix_market(path) -> SymmetricMatrix:
+    """proj/src/matrix_market.cpp:31-117 (coordinate / array, real symmetric),
+    parsed by the library's host layer; upload with DeviceMatrix."""
+    n = C.c_int()
+    p = os.fsencode(path)
+    _call(L.lib().fl_mm_read, p, C.byref(n), None, 0)
+    M = np.empty((n.value, n.value), order="F")
+    _call(L.lib().fl_mm_read, p, C.byref(n), _ptr(M), n.value)
+    return SymmetricMatrix(M)
+
+
+def write_matrix_market(A, path, format: str = "coordinate") -> None:
+    """proj/src/matrix_market.cpp:119-147 (lower triangle, %.17g)."""
+    if format not in ("coordinate", "array"):
+        raise InvalidArgument(f"write_matrix_market: unknown format '{format}'")
+    M = _as_sym(A).mat()
+    _call(L.lib().fl_mm_write, os.fsencode(path), _ptr(M), M.shape[0], M.shape[0],
+          0 if format == "coordinate" else 1)
 
 
 def _as_sym(A) -> SymmetricMatrix:
