@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=8, help="node chunks in flight (1..8)")
+    ap.add_argument("--factorization", default="lu", choices=["lu", "ldlt"],
+                    help="headline factorization of z I - A: the reference's partial-pivot LU "
+                         "(default) or the complex-symmetric LDL^T (timed beside it anyway)")
+    ap.add_argument("--no-alt", action="store_true",
+                    help="skip timing the other factorization")
     a = ap.parse_args()
     if a.steps is None:
         a.steps = 3 if a.config == 4 else 5
@@ -62,6 +67,11 @@ def parse():
 
 def filter_flops(n, p, nc):
     return nc * (8.0 / 3.0 * n ** 3 + 8.0 * n * n * p)
+
+
+def ldlt_filter_flops(n, p, nc):
+    """Complex-symmetric LDL^T filter: half the LU's factorization flops."""
+    return nc * (4.0 / 3.0 * n ** 3 + 8.0 * n * n * p)
 
 
 def peaks():
@@ -248,6 +258,7 @@ def run_b200(args, rank, world, local_rank):
     ctx = D.make_context(rank, world, local_rank)
     P.set_default_context(ctx)
     ctx.set_streams(args.streams)
+    ctx.set_factorization(args.factorization)
 
     A, vals, c = build_workload(args.config, local_rank)
     n, p, nc = c["n"], c["m0"], c["n_c"]
@@ -313,6 +324,42 @@ def run_b200(args, rank, world, local_rank):
     total_flops = filter_flops(n, p, nc) * args.steps
     value = total_flops / (ms * 1e-3) / 1e9
 
+    # the other factorization of z I - A on the same X (same timing rules):
+    # ms per application and how far its Y is from the headline's
+    alt = None
+    if not args.no_alt:
+        other = "ldlt" if args.factorization == "lu" else "lu"
+        Y_head = Y.clone()
+        ctx.set_factorization(other)
+        for _ in range(max(2, args.warmup)):  # the graph is captured on the second call
+            step()
+        ctx.sync()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        ctx.sync()
+        ms_alt = e0.elapsed_time(e1)
+        if dist:
+            ms_alt = D.max_over_ranks(ms_alt)
+        rel = (torch.linalg.norm(Y - Y_head) / torch.linalg.norm(Y_head)).item()
+        ctx.set_factorization(args.factorization)
+        fl_alt = (ldlt_filter_flops(n, p, nc) if other == "ldlt" else filter_flops(n, p, nc))
+        alt = {"factorization": other, "ms_per_step": round(ms_alt / args.steps, 3),
+               "speedup_vs_headline": round(ms / ms_alt, 4),
+               "lu_equivalent_gflops": round(filter_flops(n, p, nc) * args.steps
+                                             / (ms_alt * 1e-3) / 1e9, 3),
+               "algorithmic_gflops": round(fl_alt * args.steps / (ms_alt * 1e-3) / 1e9, 3),
+               "fraction_of_fp64_peak": round(fl_alt * args.steps / (ms_alt * 1e-3) / 1e12
+                                              / (FP64_DMMA_PEAK_TFLOPS * world), 4),
+               "y_rel_diff_vs_headline": rel,
+               "flop_convention": "LDL^T: n_c (4/3 n^3 + 8 n^2 p); LU: n_c (8/3 n^3 + 8 n^2 p)"}
+        del Y_head
+
     # e2e: pinned host buffers through the same public API (H2D of X, D2H of Y inside)
     Xh = torch.empty((p, n), dtype=torch.float64, pin_memory=True).numpy().T  # n x p, col-major
     Yh = torch.empty((p, n), dtype=torch.float64, pin_memory=True).numpy().T
@@ -352,7 +399,11 @@ def run_b200(args, rank, world, local_rank):
             torch.cuda.empty_cache()
             S = P.SymmetricMatrix(Ah)
             tts = {}
-            for cache in (False, True):  # report the cache off and on
+            runs = [(False, args.factorization), (True, args.factorization)]
+            if alt is not None:
+                runs.append((False, alt["factorization"]))
+            for cache, fac in runs:  # report the cache off and on
+                ctx.set_factorization(fac)
                 cfg = P.SolverConfig(m0=p, n_c=nc, tol=c["tol"], max_iter=c["max_iter"],
                                      cache_factorizations=cache)
                 if dist:
@@ -367,11 +418,15 @@ def run_b200(args, rank, world, local_rank):
                        "eigenpairs": len(sol.eigenvalues), "expected_inside": c["inside"],
                        "max_residual": sol.trace[-1].max_residual if sol.trace else None,
                        "factorizations": sol.accounting.factorizations}
-                if not cache:
+                if fac != args.factorization:
+                    alt["tts"] = rec
+                elif not cache:
                     tts.update(rec)
                     tts["cache_factorizations"] = False
+                    tts["factorization"] = fac
                 else:
                     tts["cached"] = rec
+            ctx.set_factorization(args.factorization)
         except Exception as e:  # report, do not hide
             tts = {"error": f"{type(e).__name__}: {e}"}
 
@@ -437,6 +492,8 @@ def run_b200(args, rank, world, local_rank):
                     for k, v in prof.items()},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * n * p, "d2h_bytes_per_step": 8 * n * p},
+        "factorization": args.factorization,
+        "alt_factorization": alt,
         "gpu_launches": int(launches),
         "cpu_baseline": cpu,
         "tts": tts,

@@ -97,6 +97,20 @@ int fl_ctx_set_streams(fl_ctx* ctx, int n);
    Single-rank contexts ignore it. */
 enum { FL_REDUCE_SUM = 0, FL_REDUCE_ORDERED = 1 };
 int fl_ctx_set_reduction(fl_ctx* ctx, int mode);
+/* how the filter factors each shifted matrix z_k I - A (per context; cached
+   factors of the other kind are rebuilt at the next application):
+   FL_FACTOR_LU (default): complex partial-pivot LU, the reference's
+   Eigen::PartialPivLU (proj/src/filterop.cpp:14);
+   FL_FACTOR_LDLT: complex-symmetric LDL^T without interchanges (SURVEY.md
+   §8(f)3): z I - A is complex symmetric with Im(z I - A) = Im(z) I positive
+   definite, so every pivot satisfies |d_j| >= Im z > 0 and no pivoting is
+   needed; the trailing updates touch only the lower triangle, half the LU's
+   8/3 n^3 flops. Results agree with the LU's to rounding (tests/
+   test_gpu_ldlt.py), not bitwise. Env FEASTLAB_FACTOR=ldlt sets it for new
+   contexts. */
+enum { FL_FACTOR_LU = 0, FL_FACTOR_LDLT = 1 };
+int fl_ctx_set_factorization(fl_ctx* ctx, int mode);
+int fl_ctx_factorization(const fl_ctx* ctx); /* the mode in effect, -1 for NULL */
 /* complex product form of the filter's DMMA GEMMs (process-wide): 1 = 3M
    (three real products per complex product, the default), 0 = 4M; mode < 0
    only queries. Returns the mode in effect. Env FEASTLAB_ZGEMM=4m|3m sets

@@ -66,6 +66,8 @@ _SIGS = {
     "fl_solve_many": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P,
                            _P, _P]),
     "fl_ctx_set_reduction": (_I, [_P, _I]),
+    "fl_ctx_set_factorization": (_I, [_P, _I]),
+    "fl_ctx_factorization": (_I, [_P]),
     "fl_ctx_profile": (_I, [_P, C.c_char_p, _P, _P, _P, _P]),
     "fl_matrix_create": (_I, [_P, _P, _I, _I, _I, _PP, _P]),
     "fl_matrix_destroy": (_I, [_P]),

@@ -150,6 +150,7 @@ struct fl_ctx {
     std::vector<cudaEvent_t> ev_panel, ev_next;
     int nstreams = 8;  // node chunks in flight (<= aux.size())
     int reduction = 0;  // FL_REDUCE_SUM / FL_REDUCE_ORDERED (multi-rank Y)
+    int factorization = 0;  // FL_FACTOR_LU / FL_FACTOR_LDLT
     // Rayleigh-Ritz scratch
     DBuf rr_nxp, rr_nxp2, s1, s2, s3, s4, s5, s6, s7, vals_d, norms_d, idx_d, chol_info, ints, cnt,
         scal;
@@ -182,6 +183,8 @@ struct fl_filter {
     // factors: cache -> one per local node; else a rotating group
     DBuf fac_re, fac_im, ipiv, perm, bad, ptab;
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
+    DBuf lt_re, lt_im;    // LDL^T: per slot, the current panel's L_kk^{-T} (64 x 64)
+    int fac_mode = -1;    // factorization the cached factors were built with
     int fac_slots = 0;
     int panel_res_rows = 4096;   // see panel_res_rows()
     int lu_panels = 2;           // LU outer block = lu_panels x 64 columns (block_panels())
@@ -197,11 +200,12 @@ struct fl_filter {
     struct GraphKey {
         const void *X, *Y, *fac, *w;
         long ldx, ldy;
-        int p, slots, ns, zmode, reduction;
+        int p, slots, ns, zmode, reduction, factorization;
         bool operator==(const GraphKey& o) const {
             return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
                    ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns &&
-                   zmode == o.zmode && reduction == o.reduction;
+                   zmode == o.zmode && reduction == o.reduction &&
+                   factorization == o.factorization;
         }
     };
     GraphKey gkey{}, gseen{};
@@ -325,8 +329,15 @@ double* scratch(DBuf& b, size_t doubles) {
 // concurrently with the rest of update k (GEMM "rest").
 //   st: wait(P_k) laswp_k  U12_k  GEMM_next_k  rec(N_k)  GEMM_rest_k
 //   sp: wait(N_{k-1})  panel_k  trinv(L_kk)  rec(P_k)
+void factor_group_ldlt(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStream_t sp,
+                       cudaEvent_t ev_panel, cudaEvent_t ev_next);
+
 void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStream_t sp,
                   cudaEvent_t ev_panel, cudaEvent_t ev_next) {
+    if (f->ctx->factorization == FL_FACTOR_LDLT) {
+        factor_group_ldlt(f, g0, G, s0, st, sp, ev_panel, ev_next);
+        return;
+    }
     fl_ctx* ctx = f->ctx;
     const int N = f->A->N, n = f->A->n;
     const long stride = (long)N * N;
@@ -445,6 +456,104 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
     launch_check_diag(F, n, G, f->kb + g0, f->bad.i(), st);  // global node index
     launch_ipiv_to_perm(ipiv, f->perm.i() + (long)s0 * N, N, G, st);
+}
+
+// Complex-symmetric LDL^T (FL_FACTOR_LDLT, ldlt.cu) of nodes [g0, g0+G) into
+// factor slots [s0, ...): same factor layout as factor_group (L, U = D L^T,
+// identity permutation), trailing updates on the lower trapezoid only.
+// Outer blocks of NPB panels with the LU's look-ahead split:
+//   sp: for panel j of the block: A[k_j:, panel j] -= L[k_j:, k_0:k_j] U[k_0:k_j, panel j]
+//       | ldlt_panel | W = A[k_j+64:, panel j] L_jj^{-T} | split (L = W D^{-1}, U = W^T)
+//                                                                      -> ev_panel
+//   st: A[c0:, c0:] -= L[c0:, block] U[block, c0:], lower tiles: the next
+//       block's columns first -> ev_next, then the remainder
+// The remainder of block b-1 (rows and columns >= c0 of block b... lower
+// tiles) never touches the rows [k0, c0) or columns [k0, c0) block b's panel
+// chain writes, so the two streams need no other ordering.
+void factor_group_ldlt(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStream_t sp,
+                       cudaEvent_t ev_panel, cudaEvent_t ev_next) {
+    fl_ctx* ctx = f->ctx;
+    const int N = f->A->N, n = f->A->n;
+    const long stride = (long)N * N;
+    ZBatch F{f->fac_re.d() + s0 * stride, f->fac_im.d() + s0 * stride, N, stride};
+    NodeShifts z{};
+    for (int b = 0; b < G; ++b) {
+        z.zr[b] = f->zr[f->kb + g0 + b];
+        z.zi[b] = f->zi[f->kb + g0 + b];
+    }
+    const int NB = N / FL_TILE;
+    const long istride = 2L * NB * FL_TILE * FL_TILE;
+    ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
+    const int T = FL_TILE;
+    const long lts = (long)T * T;
+    double* ltr = f->lt_re.d() + s0 * lts;
+    double* lti = f->lt_im.d() + s0 * lts;
+    {
+        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
+        launch_shift(f->A->d(), N, N, F, z, G, st);
+    }
+    auto E = [&](int r, int c) { return (long)c * N + r; };
+    // C[cr, cc: M x nc] -= A[ar, ac: M x K] B[br, bc: K x nc]; lower >= 0: only
+    // the tiles on or below the global diagonal (tri_s = (cc - cr) / 64)
+    auto sub = [&](int M, int nc, int K, int ar, int ac, int br, int bc, int cr, int cc,
+                   cudaStream_t s, bool lower) {
+        if (M <= 0 || nc <= 0) return;
+        ZGemm g{M, nc, K, F.re + E(ar, ac), F.im + E(ar, ac), N, stride,
+                F.re + E(br, bc), F.im + E(br, bc), N, stride,
+                F.re + E(cr, cc), F.im + E(cr, cc), N, stride};
+        const int ts = (cc - cr) / T;
+        // algorithmic work: the tiles computed
+        double tiles = 0;
+        if (lower) {
+            for (int c = 0; c < nc / T; ++c) {
+                const int lo = std::max(0, c + ts);
+                if (lo < M / T) tiles += M / T - lo;
+            }
+        } else {
+            tiles = (double)(M / T) * (nc / T);
+        }
+        Prof pr(ctx, P_ZGEMM, 8.0 * tiles * T * T * K * G, 1, s);
+        if (lower) launch_zgemm_sub_lower(g, ts, G, s);
+        else launch_zgemm_sub(g, G, s);
+    };
+    const int NPB = f->lu_panels;
+    CK(cudaEventRecord(ev_next, st));  // shift done: block 0 may start
+    for (int k0 = 0; k0 < N; k0 += NPB * T) {
+        const int np = std::min(NPB, (N - k0) / T);
+        const int c0 = k0 + np * T;
+        CK(cudaStreamWaitEvent(sp, ev_next, 0));
+        for (int j = 0; j < np; ++j) {
+            const int kj = k0 + j * T;
+            if (j > 0) sub(N - kj, T, j * T, kj, k0, k0, kj, kj, kj, sp, true);
+            {
+                Prof pr(ctx, P_PANEL, 0.0, 1, sp);
+                launch_ldlt_panel(F, kj, Inv, ltr, lti, lts, G, sp);
+            }
+            const int rows = N - kj - T;
+            if (rows > 0) {
+                ZGemm w{rows, T, T, F.re + E(kj + T, kj), F.im + E(kj + T, kj), N, stride,
+                        ltr, lti, T, lts, F.re + E(kj + T, kj), F.im + E(kj + T, kj), N, stride};
+                {
+                    Prof pr(ctx, P_TRSM, 8.0 * rows * T * T * G, 1, sp);
+                    launch_zgemm_set(w, G, sp);
+                }
+                Prof pr(ctx, P_LASWP, 0.0, 1, sp);  // the split's data movement
+                launch_ldlt_split(F, kj, kj + T, rows, G, sp);
+            }
+        }
+        CK(cudaEventRecord(ev_panel, sp));
+        CK(cudaStreamWaitEvent(st, ev_panel, 0));
+        const int rest = N - c0;
+        if (rest <= 0) break;
+        const int nxt = std::min(np * T, rest);
+        sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st, true);
+        CK(cudaEventRecord(ev_next, st));
+        sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st, true);
+    }
+    Prof pr(ctx, P_PANEL, 0.0, 3, st);
+    launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
+    launch_check_diag(F, n, G, f->kb + g0, f->bad.i(), st);
+    launch_iota_perm(f->perm.i() + (long)s0 * N, N, G, st);
 }
 
 // W_b = (z_b I - A)^{-1} X for nodes [g0, g0+G) using factor slots [s0, ...).
@@ -583,8 +692,14 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * FL_MAX_BLOCK_PANELS * slots);
         f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
+        f->lt_re.ensure(sizeof(double) * (size_t)FL_TILE * FL_TILE * slots);
+        f->lt_im.ensure(sizeof(double) * (size_t)FL_TILE * FL_TILE * slots);
         f->fac_slots = slots;
         std::fill(f->factored.begin(), f->factored.end(), 0);
+    }
+    if (f->fac_mode != ctx->factorization) {  // cached factors of the other kind
+        std::fill(f->factored.begin(), f->factored.end(), 0);
+        f->fac_mode = ctx->factorization;
     }
     f->bad.ensure(sizeof(int) * 4);
     if (!f->h_bad) CK(cudaMallocHost(&f->h_bad, sizeof(int) * 4));
@@ -691,7 +806,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         }
     };
     const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
-                                  zgemm_mode(), ctx->reduction};
+                                  zgemm_mode(), ctx->reduction, ctx->factorization};
     const bool graphable = !f->cache && !ctx->prof.on && graphs_enabled();
     if (graphable && f->gexec && f->gkey == key) {
         CK(cudaGraphLaunch(f->gexec, ctx->stream));
@@ -1067,6 +1182,8 @@ static int ctx_create_impl(int device, const void* id, int rank, int nranks, fl_
         CK(cudaMallocHost(&c->h_cnt, sizeof(unsigned long long)));
         c->rank = rank;
         c->nranks = nranks;
+        if (const char* fe = std::getenv("FEASTLAB_FACTOR"))
+            c->factorization = std::strcmp(fe, "ldlt") == 0 ? FL_FACTOR_LDLT : FL_FACTOR_LU;
         if (id != nullptr) {  // a clique (also of one rank: exercises the NCCL path)
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof(uid));
@@ -1208,6 +1325,15 @@ int fl_ctx_set_reduction(fl_ctx* ctx, int mode) {
     ctx->reduction = mode;
     return FL_OK;
 }
+
+int fl_ctx_set_factorization(fl_ctx* ctx, int mode) {
+    if (!ctx || (mode != FL_FACTOR_LU && mode != FL_FACTOR_LDLT)) return FL_INVALID_ARGUMENT;
+    CtxLock lk(ctx);
+    ctx->factorization = mode;
+    return FL_OK;
+}
+
+int fl_ctx_factorization(const fl_ctx* ctx) { return ctx ? ctx->factorization : -1; }
 
 int fl_zgemm_mode(int mode) {
     if (mode >= 0) set_zgemm_mode(mode);

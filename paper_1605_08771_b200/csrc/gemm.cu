@@ -9,6 +9,39 @@
 
 namespace fl {
 
+// Tile (bx, by) of the L-th tile of C's lower trapezoid {bx >= by + s},
+// column by column (Mt x Nt tiles). Columns c < -s are full (Mt tiles); from
+// there column f + j holds H - j tiles, H = Mt - f - s.
+FL_DEV void lower_tile(long L, int Mt, int s, int& bx, int& by) {
+    const int f = s < 0 ? -s : 0;
+    const long full = (long)f * Mt;
+    if (L < full) {
+        by = (int)(L / Mt);
+        bx = (int)(L % Mt);
+        return;
+    }
+    L -= full;
+    const long H = (long)Mt - f - s;
+    auto cum = [&](long j) { return j * H - j * (j - 1) / 2; };
+    const double b = 2.0 * H + 1.0;
+    long j = (long)((b - sqrt(fmax(b * b - 8.0 * (double)L, 0.0))) * 0.5);
+    if (j < 0) j = 0;
+    while (cum(j + 1) <= L) ++j;
+    while (j > 0 && cum(j) > L) --j;
+    by = (int)(f + j);
+    bx = (int)(f + j + s + (L - cum(j)));
+}
+
+// Number of tiles of that trapezoid (host).
+static long lower_tiles(int Mt, int Nt, int s) {
+    long t = 0;
+    for (int c = 0; c < Nt; ++c) {
+        const int lo = c + s > 0 ? c + s : 0;
+        if (lo < Mt) t += Mt - lo;
+    }
+    return t;
+}
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) dgemm_kernel(DGemm g) {
     constexpr bool AKC = TA, BKC = !TB;
@@ -103,7 +136,9 @@ __global__ void __launch_bounds__(128, FL_ZGEMM_MINB) zgemm_kernel(ZGemm g) {
     // per stage: Ar, Ai, Br, Bi
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-    const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
+    int bx = blockIdx.x, by = blockIdx.y;
+    if (g.tri) lower_tile(blockIdx.x, g.M / GB, g.tri_s, bx, by);
+    const int m0 = bx * GB, n0 = by * GB;
     const long z = blockIdx.z;
     const double* Ar = g.Ar + z * g.strideA;
     const double* Ai = g.Ai + z * g.strideA;
@@ -233,7 +268,9 @@ __global__ void __launch_bounds__(NT, MINB) zgemm3m_kernel(ZGemm g) {
     extern __shared__ __align__(16) double smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
-    const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
+    int bx = blockIdx.x, by = blockIdx.y;
+    if (g.tri) lower_tile(blockIdx.x, g.M / GB, g.tri_s, bx, by);
+    const int m0 = bx * GB, n0 = by * GB;
     const long z = blockIdx.z;
     const double* Ar = g.Ar + z * g.strideA;
     const double* Ai = g.Ai + z * g.strideA;
@@ -388,6 +425,23 @@ void launch_dgemm(const DGemm& g, bool ta, bool tb, int batch, cudaStream_t s) {
 void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0 || batch <= 0) return;
     dim3 grid(g.M / GB, g.N / GB, batch);
+    if (zgemm_mode()) {
+        launch_zgemm3m<true>(g, grid, s);
+        return;
+    }
+    const size_t sm = ZSMEM;
+    ensure_smem((const void*)zgemm_kernel<true>, sm);
+    zgemm_kernel<true><<<grid, 128, sm, s>>>(g);
+}
+
+void launch_zgemm_sub_lower(const ZGemm& g0, int tri_s, int batch, cudaStream_t s) {
+    if (g0.M <= 0 || g0.N <= 0 || g0.K <= 0 || batch <= 0) return;
+    ZGemm g = g0;
+    g.tri = true;
+    g.tri_s = tri_s;
+    const long t = lower_tiles(g.M / GB, g.N / GB, tri_s);
+    if (t <= 0) return;
+    dim3 grid((unsigned)t, 1, batch);
     if (zgemm_mode()) {
         launch_zgemm3m<true>(g, grid, s);
         return;

@@ -24,8 +24,16 @@ struct ZGemm {
     const double *Ar, *Ai; long lda; long strideA;
     const double *Br, *Bi; long ldb; long strideB;
     double *Cr, *Ci; long ldc; long strideC;
+    // lower-trapezoid mode (complex-symmetric trailing updates): only the
+    // 64x64 tiles (bx, by) of C with bx >= by + tri_s are computed (tri_s =
+    // (column origin - row origin of C) / 64), enumerated column by column
+    // on a 1-D grid (launch_zgemm_sub_lower)
+    bool tri = false;
+    int tri_s = 0;
 };
 void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s);
+// C -= A B on the lower trapezoid of C only (see ZGemm::tri_s)
+void launch_zgemm_sub_lower(const ZGemm& g, int tri_s, int batch, cudaStream_t s);
 // Complex product form of the zgemm launches: 1 = 3M (default), 0 = 4M.
 int zgemm_mode();
 void set_zgemm_mode(int mode);
@@ -88,6 +96,16 @@ void launch_node_terms(ZBatch W, int N, int P, const NodeShifts& w, int batch, d
                        long tstride, cudaStream_t s);
 void launch_ordered_sum(const double* T, long tstride, const NodeSlots& sl, int nc, int N, int P,
                         double* Y, long ldy, cudaStream_t s);
+// Complex-symmetric LDL^T without interchanges (ldlt.cu): factor the 64x64
+// diagonal block at (k0, k0) of every node (lower triangle read), write L_kk,
+// D_k, U_kk = D_k L_kk^T in place, L_kk^{-1} into Inv block k0/64 and L_kk^{-T}
+// (column-major ld 64) at ltr/lti + b*lt_stride.
+void launch_ldlt_panel(ZBatch F, int k0, ZBatch Inv, double* ltr, double* lti, long lt_stride,
+                       int batch, cudaStream_t s);
+// W = F[r0 : r0+rows, k0 : k0+64] -> L = W D_k^{-1} in place, U[k0 rows, r0 : r0+rows] = W^T.
+void launch_ldlt_split(ZBatch F, int k0, int r0, int rows, int batch, cudaStream_t s);
+// perm[b*N + i] = i
+void launch_iota_perm(int* perm, int N, int batch, cudaStream_t s);
 // |U_ii| > 0 and finite for all i < n; on failure atomicMin(bad_node, offset + b).
 void launch_check_diag(ZBatch F, int n, int batch, int offset, int* bad_node, cudaStream_t s);
 

@@ -142,6 +142,22 @@ class Context:
             raise InvalidArgument("set_reduction: mode must be 'sum' or 'ordered'")
         _check(L.lib().fl_ctx_set_reduction(self.handle, 1 if mode == "ordered" else 0), L.Err())
 
+    FACTORIZATIONS = ("lu", "ldlt")
+
+    def set_factorization(self, mode: str) -> None:
+        """How the filter factors z_k I - A: "lu" (complex partial-pivot LU, the
+        reference's PartialPivLU; default) or "ldlt" (complex-symmetric LDL^T
+        without interchanges: half the flops, pivots bounded below by Im z_k;
+        agrees with "lu" to rounding)."""
+        if mode not in self.FACTORIZATIONS:
+            raise InvalidArgument("set_factorization: mode must be 'lu' or 'ldlt'")
+        _check(L.lib().fl_ctx_set_factorization(self.handle, self.FACTORIZATIONS.index(mode)),
+               L.Err())
+
+    @property
+    def factorization(self) -> str:
+        return self.FACTORIZATIONS[L.lib().fl_ctx_factorization(self.handle)]
+
     def set_profiling(self, on: bool) -> None:
         """Per-kernel-class CUDA-event timing on the context stream."""
         L.lib().fl_ctx_set_profiling(self.handle, int(bool(on)))

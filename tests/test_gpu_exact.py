@@ -4,13 +4,24 @@ known answer). cfg3: the 96 x 96 Dirichlet Laplacian, analytic eigenpairs
 u_jk(p, q) = sin(j pi p h) sin(k pi q h), 200 inside with degenerate pairs.
 cfg4: A = Q Lambda Q^T built on the device as bench.py does (n = 16384),
 exact pairs (Lambda, Q). Gates: converged, eigenvalue count, eigenvalues to
-1e-10 of max(|lambda|), subspace sine to max(1e-8, Davis-Kahan bound)."""
+1e-10 of max(|lambda|), subspace sine to max(1e-8, Davis-Kahan bound).
+Both run with the reference's partial-pivot LU filter and with the
+complex-symmetric LDL^T one (FL_FACTOR_LDLT)."""
 import math
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["lu", "ldlt"])
+def factorization(request):
+    import paper_1605_08771_b200 as P
+    ctx = P.default_context()
+    ctx.set_factorization(request.param)
+    yield request.param
+    ctx.set_factorization("lu")
 
 
 def _laplacian_basis(m, lo, hi):
@@ -28,7 +39,7 @@ def _laplacian_basis(m, lo, hi):
     return np.asarray(lam)[order], np.stack(cols, axis=1)[:, order]
 
 
-def test_cfg3_laplacian_exact():
+def test_cfg3_laplacian_exact(factorization):
     import paper_1605_08771_b200 as P
     from paper_1605_08771_b200 import configs as CF
     c = CF.resolved(3, CF.laplacian_eigenvalues(96))
@@ -49,7 +60,7 @@ def test_cfg3_laplacian_exact():
     assert sine <= max(1e-8, R / gap), (sine, R, gap)
 
 
-def test_cfg4_exact():
+def test_cfg4_exact(factorization):
     import torch
     import paper_1605_08771_b200 as P
     from paper_1605_08771_b200 import configs as CF

@@ -1,0 +1,105 @@
+"""Complex-symmetric LDL^T filter (FL_FACTOR_LDLT, ldlt.cu):
+every contour node's z I - A factored without interchanges, lower-trapezoid
+trailing updates. Its filter must equal the oracle's (the reference's
+partial-pivot LU, proj/src/filterop.cpp:9-32,62-84) to rounding level, for
+every outer-block width and ragged sizes, cached or not, and FEAST on it must
+reproduce the golden iteration / converged counts."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def ldlt():
+    import paper_1605_08771_b200 as P
+    ctx = P.default_context()
+    ctx.set_factorization("ldlt")
+    assert ctx.factorization == "ldlt"
+    yield P
+    ctx.set_factorization("lu")
+
+
+@pytest.mark.parametrize("n,n_c", [(64, 8), (200, 8), (700, 8), (1000, 16)])
+@pytest.mark.parametrize("lu", [1, 2, 3, 4])
+def test_ldlt_filter_matches_oracle(ldlt, n, n_c, lu, monkeypatch):
+    P = ldlt
+    monkeypatch.setenv("FEASTLAB_LU_PANELS", str(lu))
+    A = O.random_symmetric(n, 17) / np.sqrt(n)
+    X = O.random_block(n, 96, 18)
+    I = (-0.35, 0.25)
+    Y = P.apply_filter(A, P.build_contour_rule(P.SearchInterval(*I), n_c), X)
+    ref = O.apply_filter(A, O.build_contour_rule(O.SearchInterval(*I), n_c), X)
+    rel = np.linalg.norm(Y - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-12, rel
+
+
+def test_ldlt_node_solve_residual(ldlt):
+    """One node (z close to the spectrum: Im z = 1e-3): the LDL^T solve's
+    backward error is at rounding level."""
+    P = ldlt
+    n = 513
+    A = O.random_symmetric(n, 5) / np.sqrt(n)
+    X = O.random_block(n, 64, 6)
+    z = complex(0.01, 1e-3)
+    rule = P.ContourRule(P.SearchInterval(-0.1, 0.1), [z], [complex(1.0, 0.0)])
+    orule = O.ContourRule(O.SearchInterval(-0.1, 0.1), [z], [complex(1.0, 0.0)])
+    Y = P.apply_filter(A, rule, X)
+    ref = O.apply_filter(A, orule, X)
+    assert np.linalg.norm(Y - ref) / np.linalg.norm(ref) <= 1e-11
+
+
+def test_ldlt_cache_and_mode_switch():
+    """Cached factors are rebuilt when the factorization mode changes; both
+    modes give the oracle's filter."""
+    import paper_1605_08771_b200 as P
+    ctx = P.default_context()
+    n = 900
+    A = O.random_symmetric(n, 21) / np.sqrt(n)
+    rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.3), 8)
+    orule = O.build_contour_rule(O.SearchInterval(-0.3, 0.3), 8)
+    f = P.FilterApplier(A, rule, True)
+    acc = P.SolveAccounting()
+    try:
+        for mode, seed in (("lu", 1), ("ldlt", 2), ("ldlt", 3), ("lu", 4)):
+            ctx.set_factorization(mode)
+            X = O.random_block(n, 40, seed)
+            Y = f.apply(X, acc)
+            ref = O.apply_filter(A, orule, X)
+            assert np.linalg.norm(Y - ref) / np.linalg.norm(ref) <= 1e-12, mode
+        # LU, LDL^T (refactor), LDL^T (cached), LU (refactor): 3 x 8 factorizations
+        assert acc.factorizations == 24
+    finally:
+        ctx.set_factorization("lu")
+
+
+def test_ldlt_invalid_mode():
+    import paper_1605_08771_b200 as P
+    with pytest.raises(P.InvalidArgument):
+        P.default_context().set_factorization("cholesky")
+
+
+def test_ldlt_first_filtered_cfg0(ldlt):
+    """The north-star first-iterate gate (1e-9 relative Frobenius) against the
+    oracle at cfg0 with the LDL^T filter."""
+    import test_gpu_configs as TC
+    TC.test_cfg0_first_filtered_subspace(TC._fixture(0))
+
+
+@pytest.mark.parametrize("index", [2, 3])
+def test_ldlt_first_filtered_vs_golden(ldlt, index):
+    """The same gate through the golden sketch and column norms at cfg2/cfg3."""
+    import test_gpu_configs as TC
+    TC.test_first_filtered_subspace_vs_golden_sketch(index, TC._fixture(0))
+
+
+@pytest.mark.parametrize("index,driver", [(0, "feast_solve"), (0, "xfeast_solve"),
+                                          (0, "rfeast_solve"), (1, "feast_solve"),
+                                          (3, "feast_solve")])
+def test_ldlt_drivers_vs_golden(ldlt, index, driver):
+    """Drivers on the LDL^T filter: the golden oracle's iteration / converged
+    counts, traces and eigenvalues (the same gates as test_gpu_configs)."""
+    import test_gpu_configs as TC
+    TC.test_drivers_vs_golden_oracle(index, driver, TC._fixture(0))
