@@ -201,11 +201,12 @@ struct fl_filter {
         const void *X, *Y, *fac, *w;
         long ldx, ldy;
         int p, slots, ns, zmode, reduction, factorization;
+        int phase;  // 0: factor + solve (no cache); cache: 1 factor + solve, 2 solve only
         bool operator==(const GraphKey& o) const {
             return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
                    ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns &&
                    zmode == o.zmode && reduction == o.reduction &&
-                   factorization == o.factorization;
+                   factorization == o.factorization && phase == o.phase;
         }
     };
     GraphKey gkey{}, gseen{};
@@ -805,18 +806,34 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
                        "ncclAllReduce(bad node)");
         }
     };
+    // Graph policy: an application is pure stream work, so it is captured and
+    // replayed while its launch key holds. Eager (host-paced) launches enqueue
+    // chunk after chunk, and once a stream's launch queue is full the host
+    // blocks on it while the other chunks' streams wait for work: cfg4's LU
+    // (54k launches) runs 13.3 s eagerly against 11.4 s as one graph, while
+    // capture + instantiate cost 0.4 s. So large problems (N >= 2048) capture
+    // on the first call; small ones on the second (their capture costs more
+    // than an eager application saves). Cached factorizations: the factoring
+    // application is captured too (launched once, phase 1), the solve-only
+    // ones are replayed (phase 2).
+    bool needs_factor = false;
+    if (f->cache)
+        for (char d : f->factored) needs_factor |= !d;
+    const int phase = f->cache ? (needs_factor ? 1 : 2) : 0;
     const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
-                                  zgemm_mode(), ctx->reduction, ctx->factorization};
-    const bool graphable = !f->cache && !ctx->prof.on && graphs_enabled();
-    if (graphable && f->gexec && f->gkey == key) {
+                                  zgemm_mode(), ctx->reduction, ctx->factorization, phase};
+    const bool graphable = !ctx->prof.on && graphs_enabled();
+    const bool big = N >= 2048;
+    if (graphable && f->gexec && f->gkey == key && phase != 1) {
         CK(cudaGraphLaunch(f->gexec, ctx->stream));
         g_launch_count += f->glaunches;
-        new_facts = f->nc;
-    } else if (graphable && f->gseen == key) {
-        if (f->gexec) {
+        new_facts = f->cache ? 0 : f->nc;
+    } else if (graphable && (f->gseen == key || big)) {
+        if (f->gexec) {  // an in-flight launch of it completes first
             cudaGraphExecDestroy(f->gexec);
             f->gexec = nullptr;
         }
+        const std::vector<char> factored0 = f->factored;
         const long long l0 = g_launch_count;
         CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
         cudaGraph_t graph = nullptr;
@@ -825,6 +842,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         } catch (...) {
             cudaStreamEndCapture(ctx->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
+            f->factored = factored0;
             throw;
         }
         CK(cudaStreamEndCapture(ctx->stream, &graph));
@@ -832,9 +850,11 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         const cudaError_t e =
             cudaGraphInstantiate(&f->gexec, graph, cudaGraphInstantiateFlagUseNodePriority);
         cudaGraphDestroy(graph);
+        if (e != cudaSuccess) f->factored = factored0;
         CK(e);
         f->glaunches = g_launch_count - l0;
         f->gkey = key;
+        f->gseen = key;
         CK(cudaGraphLaunch(f->gexec, ctx->stream));
     } else {
         f->gseen = key;

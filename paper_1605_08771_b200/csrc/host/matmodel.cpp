@@ -6,6 +6,7 @@
 #include <cmath>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace feastlab {
 
@@ -23,11 +24,15 @@ SymmetricMatrix::SymmetricMatrix(const double* entries, int n, long lda, double 
 
 void SymmetricMatrix::init(const double* e, int n, long lde, double sym_tol) {
     // 64 x 64 tile pairs (I, J <= I): both tiles are read while cache
-    // resident instead of striding through the transpose (n = 16384: seconds
-    // -> tens of milliseconds); the same max / (a + b) / 2 arithmetic
+    // resident instead of striding through the transpose, and one parallel
+    // pass both checks and writes (the destination is not pre-zeroed, so its
+    // pages are first touched here, by all threads); the same max and
+    // (a + b) / 2 arithmetic as the reference
     constexpr int T = 64;
     const int nt = (n + T - 1) / T;
     double scale = 1.0, asym = 0.0;
+    MatrixXd out(n, n, uninitialized);
+    double* m = out.data();
 #pragma omp parallel for schedule(dynamic, 1) reduction(max : scale, asym)
     for (int J = 0; J < nt; ++J)
         for (int I = J; I < nt; ++I)
@@ -36,21 +41,14 @@ void SymmetricMatrix::init(const double* e, int n, long lde, double sym_tol) {
                     const double a = e[(size_t)j * lde + i], b = e[(size_t)i * lde + j];
                     scale = std::max(scale, std::max(std::abs(a), std::abs(b)));
                     asym = std::max(asym, std::abs(a - b));
+                    const double v = 0.5 * (a + b);
+                    m[(size_t)j * n + i] = v;
+                    m[(size_t)i * n + j] = v;
                 }
     if (asym > sym_tol * scale)
         throw std::invalid_argument("SymmetricMatrix: input not symmetric (max |A - A^T| = " +
                                     std::to_string(asym) + ")");
-    mat_ = MatrixXd(n, n);
-    double* m = mat_.data();
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int J = 0; J < nt; ++J)
-        for (int I = J; I < nt; ++I)
-            for (int j = J * T; j < std::min(n, J * T + T); ++j)
-                for (int i = I * T; i < std::min(n, I * T + T); ++i) {
-                    const double v = 0.5 * (e[(size_t)j * lde + i] + e[(size_t)i * lde + j]);
-                    m[(size_t)j * n + i] = v;
-                    m[(size_t)i * n + j] = v;
-                }
+    mat_ = std::move(out);
 }
 
 }  // namespace feastlab

@@ -1,7 +1,9 @@
 """CUDA-graph replay of filter applications (capi.cu filter_apply_dev).
 
-Call 1 runs eagerly, call 2 with the same launch key is captured and
-launched, later calls replay. Every path must give bitwise the same Y as
+Small problems (N < 2048): call 1 runs eagerly, call 2 with the same launch
+key is captured and launched, later calls replay. Large ones capture on the
+first call; with cached factorizations the factoring application is captured
+and launched once, the solve-only applications are captured and replayed. Every path must give bitwise the same Y as
 the eager run, a changed key (new X buffer, new block width) must re-capture,
 and the launch counter must keep counting the replayed kernels.
 """
@@ -65,3 +67,21 @@ def test_device_buffers_replay():
         outs.append(Yd.cpu().numpy().T.copy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
     assert np.array_equal(outs[0], f.apply(X))
+
+
+def test_large_first_call_capture_and_cached_phases():
+    """N >= 2048: every call runs as a graph. Cached factors: call 1 (factor +
+    solve graph), call 2 (solve-only capture), call 3 (replay) agree bitwise
+    with each other and with the uncached filter, and factor once."""
+    P, A, X, rule = _setup(n=2100, p=64, nc=2, seed=5)
+    ctx = P.Context(0)
+    acc = P.SolveAccounting()
+    fc = P.FilterApplier(A, rule, True, ctx=ctx)
+    Yc = [fc.apply(X, acc) for _ in range(3)]
+    assert acc.factorizations == 2 and acc.rhs_solved == 3 * 2 * 64
+    f = P.FilterApplier(A, rule, ctx=ctx)
+    Y = [f.apply(X) for _ in range(2)]
+    for y in Yc[1:] + Y:
+        assert np.array_equal(y, Yc[0])
+    Yo = O.apply_filter(A, O.build_contour_rule(O.SearchInterval(-0.2, 0.3), 2), X)
+    assert np.linalg.norm(Yc[0] - Yo) / np.linalg.norm(Yo) <= 1e-12
