@@ -28,90 +28,137 @@ namespace {
 constexpr int LW = FL_TILE;  // 64
 
 struct LdltShared {
-    double Ar[LW][LW + 1];
-    double Ai[LW][LW + 1];
-    double Xr[LW][LW + 1];
-    double Xi[LW][LW + 1];
+    double Lr[LW][LW + 1];  // L (strict lower) and D, after the elimination
+    double Li[LW][LW + 1];
+    double cr[2][LW], ci[2][LW];  // broadcast column (elimination) / row (inverse)
 };
 
-// One CTA per node. 256 threads.
+// One CTA per node, 256 threads: thread (i = tid & 63, q = tid >> 6) keeps
+// row i's entries of the columns k = q + 4m (m < 16) in registers. Each
+// elimination step and each substitution step is one CTA barrier: the owners
+// of column j (row r) publish it in a double-buffered shared vector, then
+// every thread updates its 16 entries from registers.
 __global__ void __launch_bounds__(256) ldlt_panel_kernel(ZBatch F, int k0, ZBatch Inv, double* ltr,
                                                          double* lti, long lt_stride) {
     extern __shared__ __align__(16) unsigned char raw[];
     LdltShared& sh = *reinterpret_cast<LdltShared*>(raw);
+    constexpr int NM = LW / 4;
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
+    const int i = tid & (LW - 1), q = tid >> 6;
     double* Fr = F.re + b * F.stride;
     double* Fi = F.im + b * F.stride;
-    // the diagonal block's lower triangle (its upper part is stale: the
-    // trailing updates compute the lower trapezoid only)
-    for (int e = tid; e < LW * LW; e += 256) {
-        const int i = e & (LW - 1), k = e >> 6;
-        if (i >= k) {
-            const long o = (long)(k0 + k) * F.ld + k0 + i;
-            sh.Ar[i][k] = Fr[o];
-            sh.Ai[i][k] = Fi[o];
+    // the diagonal block's lower triangle, mirrored (the trailing updates
+    // computed only the lower trapezoid: the upper part is stale)
+    double ar[NM], ai[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        const int k = q + 4 * m;
+        const long o = i >= k ? (long)(k0 + k) * F.ld + k0 + i : (long)(k0 + i) * F.ld + k0 + k;
+        ar[m] = Fr[o];
+        ai[m] = Fi[o];
+    }
+    // right-looking elimination: c = column j of the Schur complement,
+    // l_i = c_i / d_j, a_ik -= l_i c_k for i, k > j -- the partial-pivot LU's
+    // update a_ik -= l_ij u_jk with u_jk = a_kj
+    // (j = 4 mj + qj with mj unrolled: the published entry ar[mj] has a
+    // static index, so the row stays in registers)
+#pragma unroll
+    for (int mj = 0; mj < NM; ++mj) {
+#pragma unroll 1
+        for (int qj = 0; qj < 4; ++qj) {
+            const int j = 4 * mj + qj;
+            if (j == LW - 1) break;
+            const int buf = j & 1;
+            if (q == qj) {
+                sh.cr[buf][i] = ar[mj];
+                sh.ci[buf][i] = ai[mj];
+            }
+            __syncthreads();
+            if (i > j) {
+                const cplx inv = crecip(cplx{sh.cr[buf][j], sh.ci[buf][j]});
+                const cplx l = cmul(cplx{sh.cr[buf][i], sh.ci[buf][i]}, inv);
+#pragma unroll
+                for (int m = 0; m < NM; ++m) {
+                    const int k = q + 4 * m;
+                    if (k > j) {
+                        const double cr = sh.cr[buf][k], ci = sh.ci[buf][k];
+                        ar[m] -= l.re * cr - l.im * ci;
+                        ai[m] -= l.re * ci + l.im * cr;
+                    } else if (k == j) {
+                        ar[m] = l.re;
+                        ai[m] = l.im;
+                    }
+                }
+            }
         }
-        sh.Xr[i][k] = (i == k) ? 1.0 : 0.0;
-        sh.Xi[i][k] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        const int k = q + 4 * m;
+        if (i >= k) {
+            sh.Lr[i][k] = ar[m];
+            sh.Li[i][k] = ai[m];
+        }
     }
     __syncthreads();
-    // right-looking elimination on the lower triangle: column j of the Schur
-    // complement c_i = a_ij, l_i = c_i / d_j, a_ik -= l_i c_k (i >= k > j) --
-    // the partial-pivot LU's update a_ik -= l_ij u_jk with u_jk = a_kj
-    for (int j = 0; j < LW - 1; ++j) {
-        const cplx inv = crecip(cplx{sh.Ar[j][j], sh.Ai[j][j]});
-        for (int e = tid; e < LW * LW; e += 256) {
-            const int i = e & (LW - 1), k = e >> 6;
-            if (k > j && i >= k) {
-                const cplx l = cmul(cplx{sh.Ar[i][j], sh.Ai[i][j]}, inv);
-                const cplx c{sh.Ar[k][j], sh.Ai[k][j]};
-                sh.Ar[i][k] -= l.re * c.re - l.im * c.im;
-                sh.Ai[i][k] -= l.re * c.im + l.im * c.re;
+    // X = L^{-1} (unit lower), thread (i, q) holding X[i][q + 4m]: row r is
+    // final after step r - 1; its owners publish it, rows below subtract
+    // L[i][r] X[r][:] (only columns k <= r are non-zero)
+    double xr[NM], xi[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        xr[m] = (q + 4 * m == i) ? 1.0 : 0.0;
+        xi[m] = 0.0;
+    }
+#pragma unroll 1
+    for (int r = 0; r < LW - 1; ++r) {
+        const int buf = r & 1;
+        if (i == r) {
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                sh.cr[buf][q + 4 * m] = xr[m];
+                sh.ci[buf][q + 4 * m] = xi[m];
             }
         }
         __syncthreads();
-        if (tid > j && tid < LW) {
-            const cplx l = cmul(cplx{sh.Ar[tid][j], sh.Ai[tid][j]}, inv);
-            sh.Ar[tid][j] = l.re;
-            sh.Ai[tid][j] = l.im;
+        if (i > r) {
+            const cplx l{sh.Lr[i][r], sh.Li[i][r]};
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                const int k = q + 4 * m;
+                if (k <= r) {
+                    const double cr = sh.cr[buf][k], ci = sh.ci[buf][k];
+                    xr[m] -= l.re * cr - l.im * ci;
+                    xi[m] -= l.re * ci + l.im * cr;
+                }
+            }
         }
-        __syncthreads();
-    }
-    // X = L^{-1} (unit lower) by forward substitution on the identity:
-    // thread (col = tid & 63, q = tid >> 6) owns rows q, q + 4, ...
-    const int col = tid & 63, q = tid >> 6;
-    for (int r = 0; r < LW - 1; ++r) {
-        const cplx x{sh.Xr[r][col], sh.Xi[r][col]};
-        for (int i = r + 1 + ((q - r - 1) & 3); i < LW; i += 4) {
-            const cplx l{sh.Ar[i][r], sh.Ai[i][r]};
-            sh.Xr[i][col] -= l.re * x.re - l.im * x.im;
-            sh.Xi[i][col] -= l.re * x.im + l.im * x.re;
-        }
-        __syncthreads();
     }
     double* Ir = Inv.re + b * Inv.stride + (long)(k0 / LW) * LW * LW;
     double* Ii = Inv.im + b * Inv.stride + (long)(k0 / LW) * LW * LW;
     double* Tr = ltr + b * lt_stride;
     double* Ti = lti + b * lt_stride;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+        const int k = q + 4 * m;
+        Ir[(long)k * LW + i] = xr[m];  // L^{-1}, column-major ld 64
+        Ii[(long)k * LW + i] = xi[m];
+        Tr[(long)i * LW + k] = xr[m];  // L^{-T}
+        Ti[(long)i * LW + k] = xi[m];
+    }
+    // the factor's diagonal block: L below, D on, U = D L^T above the diagonal
     for (int e = tid; e < LW * LW; e += 256) {
-        const int i = e & (LW - 1), k = e >> 6;
-        const long o = (long)(k0 + k) * F.ld + k0 + i;
-        double vr, vi;
-        if (i >= k) {  // L (strict lower) and D
-            vr = sh.Ar[i][k];
-            vi = sh.Ai[i][k];
-        } else {  // U_ik = d_i l_ki
-            const cplx u = cmul(cplx{sh.Ar[i][i], sh.Ai[i][i]}, cplx{sh.Ar[k][i], sh.Ai[k][i]});
-            vr = u.re;
-            vi = u.im;
+        const int r = e & (LW - 1), c = e >> 6;
+        const long o = (long)(k0 + c) * F.ld + k0 + r;
+        if (r >= c) {
+            Fr[o] = sh.Lr[r][c];
+            Fi[o] = sh.Li[r][c];
+        } else {  // U_rc = d_r l_cr
+            const cplx u = cmul(cplx{sh.Lr[r][r], sh.Li[r][r]}, cplx{sh.Lr[c][r], sh.Li[c][r]});
+            Fr[o] = u.re;
+            Fi[o] = u.im;
         }
-        Fr[o] = vr;
-        Fi[o] = vi;
-        Ir[(long)k * LW + i] = sh.Xr[i][k];  // L^{-1}, column-major ld 64
-        Ii[(long)k * LW + i] = sh.Xi[i][k];
-        Tr[(long)k * LW + i] = sh.Xr[k][i];  // L^{-T}
-        Ti[(long)k * LW + i] = sh.Xi[k][i];
     }
 }
 

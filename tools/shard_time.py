@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--gpus", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--factorization", default="lu", choices=["lu", "ldlt"])
     args = ap.parse_args()
     import torch
 
@@ -40,6 +41,7 @@ def main():
     A = (A + A.T) * (0.5 / n ** 0.5)
     ctx = P.default_context()
     ctx.set_streams(args.streams)
+    ctx.set_factorization(args.factorization)
     dA = P.DeviceMatrix.from_device(A.data_ptr(), n, n, ctx)
     X = torch.randn(p, n, dtype=torch.float64, device=dev, generator=g)
     Y = torch.empty_like(X)
@@ -62,8 +64,8 @@ def main():
         ms = e0.elapsed_time(e1) / args.steps
         if base is None:
             base = ms * G  # the first entry's shard time scaled to all n_c nodes
-        flops = k * (8.0 / 3.0 * n ** 3 + 8.0 * n * n * p)
-        print(json.dumps({"config": args.config, "gpus": G, "nodes_per_gpu": k,
+        flops = k * ((8.0 if args.factorization == "lu" else 4.0) / 3.0 * n ** 3 + 8.0 * n * n * p)
+        print(json.dumps({"config": args.config, "factorization": args.factorization, "gpus": G, "nodes_per_gpu": k,
                           "ms_per_step": round(ms, 3), "tflops_per_gpu": round(flops / ms / 1e9, 2),
                           "speedup_vs_1": round(base / ms, 2)}),
               flush=True)
