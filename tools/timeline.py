@@ -7,6 +7,8 @@ from paper_1605_08771_b200 import _lib
 n, p, nc = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 streams = int(sys.argv[4]) if len(sys.argv) > 4 else 4
 ctx = P.default_context()
+if len(sys.argv) > 5:
+    ctx.set_factorization(sys.argv[5])
 A = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n))); A = 0.5 * (A + A.T) / np.sqrt(n)
 X = np.asfortranarray(np.random.default_rng(1).standard_normal((n, p)))
 f = P.FilterApplier(A, P.build_contour_rule(P.SearchInterval(-0.3, 0.2), nc), ctx=ctx)
@@ -54,3 +56,10 @@ if len(z):
         if m.any():
             print(f"    work [{lo:.0e},{hi:.0e}): {m.sum():4d} launches, {dur[m].sum():7.2f} ms, "
                   f"{w[m].sum()/dur[m].sum()/1e9:6.2f} TF/s")
+
+perm = rec[rec[:, 0] == 5]
+pan = rec[rec[:, 0] == 1]
+if len(perm) and len(pan):
+    print(f"  factor phase ends {perm[:, 1].min():.2f} ms (first solve starts), last panel ends "
+          f"{pan[:, 2].max():.2f} ms, span {T:.2f} ms; panel launches {len(pan)}, "
+          f"mean panel {np.mean(pan[:, 2] - pan[:, 1]) * 1e3:.1f} us")
