@@ -76,7 +76,11 @@ __global__ void __launch_bounds__(256) ldlt_panel_kernel(ZBatch F, int k0, ZBatc
             }
             __syncthreads();
             if (i > j) {
-                const cplx inv = crecip(cplx{sh.cr[buf][j], sh.ci[buf][j]});
+                // 1/d = conj(d) / |d|^2: one reciprocal on the step's critical
+                // path (|d| >= Im z, so no scaling is needed)
+                const double dr = sh.cr[buf][j], di = sh.ci[buf][j];
+                const double s2 = 1.0 / (dr * dr + di * di);
+                const cplx inv{dr * s2, -di * s2};
                 const cplx l = cmul(cplx{sh.cr[buf][i], sh.ci[buf][i]}, inv);
 #pragma unroll
                 for (int m = 0; m < NM; ++m) {
