@@ -266,6 +266,7 @@ def run_b200(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     X = torch.from_numpy(np.ascontiguousarray(X0.T)).to(dev)   # (p, n) row-major == n x p col-major
     Y = torch.empty((p, n), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()  # X on torch's stream; the library reads it on its own
     dA = P.DeviceMatrix.from_device(A.data_ptr(), n, n, ctx)
     rule = P.build_contour_rule(P.SearchInterval(c["lo"], c["hi"]), nc)
     filt = P.FilterApplier(None, rule, False, ctx=ctx, device_matrix=dA)

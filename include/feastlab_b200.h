@@ -132,7 +132,11 @@ int fl_ctx_profile(fl_ctx* ctx, const char* cls, double* ms, double* work, long 
 
 /* ------------------------------------------------------------ matrix
    SymmetricMatrix (proj/include/feastlab/matmodel.hpp:12-24): the caller has
-   already symmetrised (fl_symmetric_matrix); the device copy is zero-padded. */
+   already symmetrised (fl_symmetric_matrix); the device copy is zero-padded.
+   loc = FL_DEVICE: A may still be being written on another stream; the copy
+   waits for the device first. (Device-resident X of fl_block_set /
+   fl_filter_apply_raw must be complete before the call: they are ordered on
+   the context stream only.) */
 int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_matrix** out,
                      fl_err* err);
 int fl_matrix_destroy(fl_matrix* m);

@@ -1416,6 +1416,9 @@ int fl_matrix_create(fl_ctx* ctx, const double* A, int n, int lda, int loc, fl_m
         m->N = round_up(n, FL_TILE);
         m->buf.ensure(sizeof(double) * (size_t)m->N * m->N);
         CK(cudaMemsetAsync(m->buf.p, 0, sizeof(double) * (size_t)m->N * m->N, ctx->stream));
+        // a device-resident A may still be in flight on the producer's stream
+        // (e.g. torch's): the one-time copy waits for the whole device
+        if (loc == FL_DEVICE) CK(cudaDeviceSynchronize());
         copy_in(ctx, m->d(), m->N, n, A, lda, n, loc);
         sync(ctx);
         ctx_retain(ctx);

@@ -86,3 +86,42 @@ def test_cfg4_exact(factorization):
     gap = np.abs(sol.eigenvalues[:, None] - vals[~inside][None, :]).min()
     R = max(sol.residual_norms) * np.sqrt(len(sol.eigenvalues))
     assert sine <= max(1e-8, R / gap), (sine, R, gap)
+
+
+def test_cfg4_first_filtered_known_answer(factorization):
+    """North-star first-iterate gate at cfg4 (no oracle golden: the CPU
+    oracle needs ~25 min of 16 cores per application there). With A =
+    Q diag(lambda) Q^T, the filter the reference applies
+    (filterop.cpp:62-84) is exactly Y1 = Q diag(rho(lambda)) Q^T X0 with
+    rho(lambda) = sum_k Re(w_k / (z_k - lambda)) (contour.cpp:83-88), so the
+    reference's own Y1 lies within its solve rounding (~cond * eps ~ 1e-12)
+    of that; the B200 Y1 must be within 1e-9 relative Frobenius of it."""
+    import torch
+    import paper_1605_08771_b200 as P
+    from paper_1605_08771_b200 import configs as CF
+    vals = CF.spectrum(4, P.uniform_values)
+    c = CF.resolved(4, vals)
+    n, p = c["n"], c["m0"]
+    dev = torch.device("cuda", 0)
+    G = torch.from_numpy(P.gaussian_block(n, n, 1004)).to(dev)
+    Q, _ = torch.linalg.qr(G)
+    del G
+    A = (Q * torch.from_numpy(vals).to(dev)) @ Q.T
+    A = (0.5 * (A + A.T)).contiguous()
+    ctx = P.default_context()
+    dA = P.DeviceMatrix.from_device(A.data_ptr(), n, n, ctx)
+    X0 = P.make_initial_guess(n, p, 42)
+    X = torch.from_numpy(np.ascontiguousarray(X0.T)).to(dev)  # (p, n) row-major == n x p
+    Y = torch.empty_like(X)
+    rule = P.build_contour_rule(P.SearchInterval(c["lo"], c["hi"]), c["n_c"])
+    f = P.FilterApplier(None, rule, False, ctx=ctx, device_matrix=dA)
+    torch.cuda.synchronize()
+    f.apply_device(X.data_ptr(), n, p, Y.data_ptr(), n)
+    ctx.sync()
+    rho = torch.tensor([P.filter_value(rule, float(l)) for l in vals], dtype=torch.float64,
+                       device=dev)
+    Xc = X.T  # n x p
+    Y_exact = Q @ (rho[:, None] * (Q.T @ Xc))
+    rel = (torch.linalg.norm(Y.T - Y_exact) / torch.linalg.norm(Y_exact)).item()
+    print(f"cfg4 {factorization}: ||Y1 - Q rho(L) Q^T X0|| / ||.|| = {rel:.2e}")
+    assert rel <= 1e-9
