@@ -31,7 +31,7 @@ namespace {
 using namespace fl;
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
-constexpr int FL_MAX_BLOCK_PANELS = 4;
+constexpr int FL_MAX_BLOCK_PANELS = 8;
 
 struct Fail {
     int code;
@@ -642,9 +642,9 @@ int panel_res_rows(int local_nodes) {
     return local_nodes <= few ? 4096 : thr;
 }
 
-// Panels per LU outer block / tiles per triangular-solve row block (1..4).
-// Many local nodes (throughput-bound): 4, so the trailing updates run with
-// K = 256; few (latency-bound: the per-node panel chain sets the step time):
+// Panels per LU outer block / tiles per triangular-solve row block (1..8).
+// Many local nodes (throughput-bound): 4 (8 when N >= 12288), so the trailing
+// updates run with K = 256 (512); few (latency-bound: the per-node panel chain sets the step time):
 // 2, so the look-ahead stream has half as many panels to factor per block.
 int block_panels(const char* env, int dflt) {
     const char* e = std::getenv(env);
@@ -708,7 +708,9 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
     const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
     f->panel_res_rows = panel_res_rows(L);
-    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? 4 : 2);
+    // 8 panels (K = 512 trailing updates) pay off only on large matrices
+    // (cfg4: -2 %; cfg2 at n = 4096: +24 %, the longer in-block chain)
+    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? (N >= 12288 ? 8 : 4) : 2);
     f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4);
     long long new_facts = 0;
     // everything below is stream work only (no host synchronisation), so a

@@ -1,8 +1,9 @@
 """LU outer-block and triangular-solve block widths (FEASTLAB_LU_PANELS,
-FEASTLAB_SOLVE_PANELS: 1..4 panels / tiles of 64): every width, including
+FEASTLAB_SOLVE_PANELS: 1..8 panels / tiles of 64): every width, including
 ragged last blocks (N / 64 not a multiple of the width), gives the oracle's
-filter (proj/src/filterop.cpp:62-84) to rounding level. The defaults pick 4
-panels (K = 256 trailing updates) for >= 8 local nodes and 2 below."""
+filter (proj/src/filterop.cpp:62-84) to rounding level. The defaults pick 8
+panels (K = 512 trailing updates) for >= 8 local nodes of N >= 12288, 4 for
+>= 8 local nodes of smaller N, and 2 below."""
 import os
 
 import numpy as np
@@ -14,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("n,n_c", [(700, 8), (1000, 16)])
-@pytest.mark.parametrize("lu,solve", [(1, 1), (2, 2), (3, 3), (4, 4), (4, 1), (1, 4), (3, 2)])
+@pytest.mark.parametrize("lu,solve", [(1, 1), (2, 2), (3, 3), (4, 4), (4, 1), (1, 4), (3, 2),
+                                      (8, 8), (6, 3), (7, 5)])
 def test_block_widths_match_oracle(n, n_c, lu, solve, monkeypatch):
     import paper_1605_08771_b200 as P
     monkeypatch.setenv("FEASTLAB_LU_PANELS", str(lu))

@@ -23,7 +23,7 @@ def ldlt():
 
 
 @pytest.mark.parametrize("n,n_c", [(64, 8), (200, 8), (700, 8), (1000, 16)])
-@pytest.mark.parametrize("lu", [1, 2, 3, 4])
+@pytest.mark.parametrize("lu", [1, 2, 3, 4, 6, 8])
 def test_ldlt_filter_matches_oracle(ldlt, n, n_c, lu, monkeypatch):
     P = ldlt
     monkeypatch.setenv("FEASTLAB_LU_PANELS", str(lu))
