@@ -204,6 +204,15 @@ def cpu_sample(c, threads):
     return flops / dt / 1e9, dt, n
 
 
+def workload_config(args, c, world):
+    """The bench line's config object, identical for both arms."""
+    n, p, nc = c["n"], c["m0"], c["n_c"]
+    return {"workload": f"cfg{args.config}", "name": f"{n}x{n} dense, m0={p}, n_c={nc}",
+            "n": n, "m0": p, "n_c": nc, "interval": [c["lo"], c["hi"]],
+            "parallelism": f"contour nodes sharded {nc}/{world} per GPU + NCCL allreduce",
+            "l2": "inputs larger than L2 (n_c LU factors, 16 n^2 B each)"}
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -229,8 +238,7 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t_all / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic",
-        "config": {"workload": CF.CONFIGS[args.config].name, "n": c["n"], "m0": c["m0"],
-                   "n_c": c["n_c"]},
+        "config": workload_config(args, c, world),
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
                          "kind": "port",
                          "sample": f"one contour node per step (zI-A LU + m0-RHS solve + "
@@ -464,10 +472,7 @@ def run_b200(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128/f64 (DMMA m8n8k4 f64)", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}", "name": f"{n}x{n} dense, m0={p}, n_c={nc}",
-                   "n": n, "m0": p, "n_c": nc, "interval": [c["lo"], c["hi"]],
-                   "parallelism": f"contour nodes sharded {nc}/{world} per GPU + NCCL allreduce",
-                   "l2": "inputs larger than L2 (n_c LU factors, 16 n^2 B each)"},
+        "config": workload_config(args, c, world),
         "fraction_of_fp64_peak": round(value / 1e3 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
         "roofline": {"kernel": f"zgemm{'3m' if mode == '3m' else ''}_kernel (DMMA; LU trailing "
                                "update, U12 and blocked solves)",
