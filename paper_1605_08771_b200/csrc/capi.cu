@@ -354,7 +354,7 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     const long istride = 2L * NB * FL_TILE * FL_TILE;
     ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
     {
-        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
+        Prof pr(ctx, P_SHIFT, (8.0 + 16.0 * G) * N * N, 1, st);
         launch_shift(f->A->d(), N, N, F, z, G, st);
     }
     const int T = FL_TILE;
@@ -490,7 +490,7 @@ void factor_group_ldlt(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cud
     double* ltr = f->lt_re.d() + s0 * lts;
     double* lti = f->lt_im.d() + s0 * lts;
     {
-        Prof pr(ctx, P_SHIFT, 24.0 * N * N * G, 1, st);
+        Prof pr(ctx, P_SHIFT, (8.0 + 16.0 * G) * N * N, 1, st);
         launch_shift(f->A->d(), N, N, F, z, G, st);
     }
     auto E = [&](int r, int c) { return (long)c * N + r; };

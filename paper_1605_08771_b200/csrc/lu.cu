@@ -1,13 +1,15 @@
 // Complex partial-pivot LU of z I - A and the blocked multi-RHS solve
 // (NodeFactorization, proj/src/filterop.cpp:9-32), batched over contour nodes.
 //
-//  shift        F = z I - A                          HBM stream, 24 N^2 B / node
+//  shift        F = z I - A                          HBM stream, (8 + 16 G) N^2 B / G nodes
 //  panel        64-wide panel, partial pivoting      panel.cu (8-CTA cluster,
 //                                                    register-resident leaves)
 //  laswp        row interchanges outside the panel   one gather/scatter per panel
 //  trinv        64x64 diagonal-block inverses        triangular solves become GEMMs
 //  zgemm        trailing update / solve updates      DMMA (gemm.cu)
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 
 #include <mutex>
 #include <map>
@@ -34,31 +36,37 @@ void ensure_smem(const void* func, size_t bytes) {
 }
 
 // ------------------------------------------------------------------ shift
-__global__ void shift_kernel(const double* __restrict__ A, long lda, int N, ZBatch F,
-                             NodeShifts z) {
-    const int b = blockIdx.y;
-    double* Fr = F.re + b * F.stride;
-    double* Fi = F.im + b * F.stride;
-    const long total = (long)N * N;
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (long)gridDim.x * blockDim.x) {
-        const long c = e / N, r = e - c * N;
-        double a = -A[c * lda + r];
-        double im = 0.0;
-        if (r == c) {
-            a += z.zr[b];
-            im = z.zi[b];
+// One thread per row pair of a column: A's pair is read once (16-byte load)
+// and written, negated and shifted, into every node of the batch (16-byte
+// stores per plane), so a launch moves 8 N^2 + 16 N^2 G bytes. Rows are the
+// fast grid axis (blockIdx.x), columns blockIdx.y: no 64-bit index division.
+__global__ void __launch_bounds__(256) shift_kernel(const double* __restrict__ A, long lda, int N,
+                                                    ZBatch F, NodeShifts z, int batch) {
+    const int c = blockIdx.y;
+    const int r = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (r >= N) return;
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(A + (long)c * lda + r));
+    const long o = (long)c * F.ld + r;
+    const int d = c - r;  // 0 or 1: the diagonal element of this pair, if any
+    for (int b = 0; b < batch; ++b) {
+        double2 re = make_double2(-a.x, -a.y), im = make_double2(0.0, 0.0);
+        if (d == 0) {
+            re.x += z.zr[b];
+            im.x = z.zi[b];
+        } else if (d == 1) {
+            re.y += z.zr[b];
+            im.y = z.zi[b];
         }
-        Fr[c * F.ld + r] = a;
-        Fi[c * F.ld + r] = im;
+        *reinterpret_cast<double2*>(F.re + b * F.stride + o) = re;
+        *reinterpret_cast<double2*>(F.im + b * F.stride + o) = im;
     }
 }
 
 void launch_shift(const double* A, long lda, int N, ZBatch F, const NodeShifts& z, int batch,
                   cudaStream_t s) {
-    int blocks = 148 * 4 / (batch > 0 ? batch : 1);
-    if (blocks < 8) blocks = 8;
-    shift_kernel<<<dim3(blocks, batch), 256, 0, s>>>(A, lda, N, F, z);
+    if (N <= 0 || batch <= 0) return;
+    // N is a multiple of the 64-wide tile; lda, F.ld even and A 16-byte aligned
+    shift_kernel<<<dim3((N / 2 + 255) / 256, N), 256, 0, s>>>(A, lda, N, F, z, batch);
 }
 
 // ------------------------------------------------------------------ panel
@@ -108,14 +116,71 @@ __global__ void __launch_bounds__(256) laswp_panel_kernel(ZBatch F, int a0, int 
     }
 }
 
+// Warp-per-column form: lane l moves entries l, l+32, l+64, l+96 of the net
+// permutation for WC columns, every load of the warp issued (8 WC in flight
+// per lane, no shared-memory round trip) before its stores; columns are
+// independent, so a __syncwarp orders the gather before the scatter.
+constexpr int LW_WC = 2;  // columns per warp
+__global__ void __launch_bounds__(256) laswp_warp_kernel(ZBatch F, int a0, int a1, int b0, int b1,
+                                                         const int* __restrict__ ptab) {
+    const int b = blockIdx.y, lane = threadIdx.x & 31;
+    const int* tab = ptab + (long)b * (4 * PW + 1);
+    const int cnt = __ldg(tab);
+    int pos[4], src[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int m = lane + 32 * q;
+        pos[q] = m < cnt ? __ldg(tab + 1 + m) : 0;
+        src[q] = m < cnt ? __ldg(tab + 1 + 2 * PW + m) : 0;
+    }
+    const int na = a1 - a0, ncols = na + (b1 - b0);
+    const int k0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LW_WC;
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    long cb[LW_WC];
+#pragma unroll
+    for (int w = 0; w < LW_WC; ++w) {
+        const int k = k0 + w;
+        cb[w] = k < ncols ? (long)(k < na ? a0 + k : b0 + (k - na)) * F.ld : -1;
+    }
+    double vr[LW_WC][4], vi[LW_WC][4];
+#pragma unroll
+    for (int w = 0; w < LW_WC; ++w)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (cb[w] >= 0 && lane + 32 * q < cnt) {
+                vr[w][q] = Fr[cb[w] + src[q]];
+                vi[w][q] = Fi[cb[w] + src[q]];
+            }
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < LW_WC; ++w)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (cb[w] >= 0 && lane + 32 * q < cnt) {
+                Fr[cb[w] + pos[q]] = vr[w][q];
+                Fi[cb[w] + pos[q]] = vi[w][q];
+            }
+}
+
 void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int batch,
                   cudaStream_t s) {
     a1 = a1 > a0 ? a1 : a0;
     b1 = b1 > b0 ? b1 : b0;
     const int ncols = (a1 - a0) + (b1 - b0);
     if (ncols <= 0) return;
-    laswp_panel_kernel<<<dim3((ncols + LS_COLS - 1) / LS_COLS, batch), 256, 0, s>>>(F, a0, a1, b0,
-                                                                                   b1, ptab);
+    static const bool smem_form = [] {
+        const char* e = std::getenv("FEASTLAB_LASWP");
+        return e && std::strcmp(e, "smem") == 0;
+    }();
+    if (smem_form) {
+        laswp_panel_kernel<<<dim3((ncols + LS_COLS - 1) / LS_COLS, batch), 256, 0, s>>>(
+            F, a0, a1, b0, b1, ptab);
+        return;
+    }
+    constexpr int per_cta = 8 * LW_WC;
+    laswp_warp_kernel<<<dim3((ncols + per_cta - 1) / per_cta, batch), 256, 0, s>>>(F, a0, a1, b0,
+                                                                                  b1, ptab);
 }
 
 // ------------------------------------------------------------------ 64x64 triangular inverses
@@ -251,24 +316,24 @@ void launch_permute_rhs(const double* X, long ldx, int N, int P, const int* perm
 // exactly as proj/src/filterop.cpp:80 evaluates it.
 __global__ void accumulate_kernel(ZBatch W, int N, int P, NodeShifts w, int batch, double* Y,
                                   long ldy, bool add) {
-    const long total = (long)N * P;
-    for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (long)gridDim.x * blockDim.x) {
-        const long c = e / N, r = e - c * N;
-        double y = add ? Y[c * ldy + r] : 0.0;
-        for (int b = 0; b < batch; ++b) {
-            const long o = b * W.stride + c * W.ld + r;
-            const double t = __dsub_rn(__dmul_rn(w.zr[b], W.re[o]), __dmul_rn(w.zi[b], W.im[o]));
-            y = __dadd_rn(y, t);
-        }
-        Y[c * ldy + r] = y;
+    const int c = blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= N) return;
+    double y = add ? Y[(long)c * ldy + r] : 0.0;
+    const long oc = (long)c * W.ld + r;
+    for (int b = 0; b < batch; ++b) {
+        const long o = b * W.stride + oc;
+        const double t = __dsub_rn(__dmul_rn(w.zr[b], __ldcs(W.re + o)),
+                                   __dmul_rn(w.zi[b], __ldcs(W.im + o)));
+        y = __dadd_rn(y, t);
     }
+    Y[(long)c * ldy + r] = y;
 }
 
 void launch_accumulate(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* Y, long ldy,
                        bool add_to_Y, cudaStream_t s) {
-    if (P <= 0) return;
-    accumulate_kernel<<<148 * 4, 256, 0, s>>>(W, N, P, w, batch, Y, ldy, add_to_Y);
+    if (P <= 0 || N <= 0) return;
+    accumulate_kernel<<<dim3((N + 255) / 256, P), 256, 0, s>>>(W, N, P, w, batch, Y, ldy, add_to_Y);
 }
 
 // G-invariant reduction (fl_ctx_set_reduction ORDERED): every rank writes its
