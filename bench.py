@@ -464,7 +464,15 @@ def run_b200(args, rank, world, local_rank):
             rate, dt, ns = cpu_sample(c, threads)
             cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
                    "sample": f"one contour node (n={ns}, m0={p}) of the workload: LU + solve + "
-                             f"accumulate in {dt:.2f} s, oracle restatement on OpenBLAS"}
+                             f"accumulate in {dt:.2f} s, oracle restatement on OpenBLAS",
+                   # the full application at this config, extrapolated
+                   # from the sampled rate (an n^3 LU dominates both)
+                   "extrapolated_ms_per_step": round(filter_flops(n, p, nc) / (rate * 1e9) * 1e3,
+                                                     1)}
+            # and on one core (a smaller node keeps it to a few seconds)
+            r1, dt1, n1 = cpu_sample(dict(c, n=min(c["n"], 2048)), 1)
+            cpu["one_core"] = {"value": round(r1, 3), "unit": "GFLOP/s", "cores": 1,
+                               "sample": f"one contour node (n={n1}, m0={p}) in {dt1:.2f} s"}
         except Exception as e:
             cpu = {"error": f"{type(e).__name__}: {e}"}
     line = {

@@ -31,7 +31,7 @@ namespace {
 using namespace fl;
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
-constexpr int FL_MAX_BLOCK_PANELS = 8;
+constexpr int FL_MAX_BLOCK_PANELS = 16;  // LU outer block; solve row blocks <= 8
 
 struct Fail {
     int code;
@@ -642,14 +642,15 @@ int panel_res_rows(int local_nodes) {
     return local_nodes <= few ? 4096 : thr;
 }
 
-// Panels per LU outer block / tiles per triangular-solve row block (1..8).
-// Many local nodes (throughput-bound): 4 (8 when N >= 12288), so the trailing
-// updates run with K = 256 (512); few (latency-bound: the per-node panel chain sets the step time):
+// Panels per LU outer block (1..16) / tiles per triangular-solve row block (1..8).
+// Many local nodes (throughput-bound): 4 (16 when N >= 12288), so the trailing
+// updates run with K = 256 (1024; cfg4 LU 11.36 -> 11.21 s, LDL^T 5.48 -> 5.39 s
+// against 8 panels); few (latency-bound: the per-node panel chain sets the step time):
 // 2, so the look-ahead stream has half as many panels to factor per block.
-int block_panels(const char* env, int dflt) {
+int block_panels(const char* env, int dflt, int most) {
     const char* e = std::getenv(env);
     const int v = e ? std::atoi(e) : dflt;
-    return std::max(1, std::min(FL_MAX_BLOCK_PANELS, v));
+    return std::max(1, std::min(most, v));
 }
 
 size_t free_bytes() {
@@ -710,8 +711,9 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     f->panel_res_rows = panel_res_rows(L);
     // 8 panels (K = 512 trailing updates) pay off only on large matrices
     // (cfg4: -2 %; cfg2 at n = 4096: +24 %, the longer in-block chain)
-    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? (N >= 12288 ? 8 : 4) : 2);
-    f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4);
+    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? (N >= 12288 ? 16 : 4) : 2,
+                                 FL_MAX_BLOCK_PANELS);
+    f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4, 8);
     long long new_facts = 0;
     // everything below is stream work only (no host synchronisation), so a
     // non-cache application is one CUDA graph: ~2.8k launches on 9 streams
