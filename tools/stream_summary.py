@@ -35,6 +35,8 @@ def main():
     agg = collections.OrderedDict()
     for p in paths:
         for e in per_launch(p):
+            if e["kernel"].startswith("at::"):  # torch fixture kernels (building A)
+                continue
             a = agg.setdefault(e["kernel"], collections.Counter())
             a["launches"] += 1
             a["ns"] += e["gpu__time_duration.sum"]
