@@ -709,8 +709,9 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // chunk's latency-bound panels overlap another chunk's DMMA GEMMs.
     const int ns = std::max(1, std::min(std::min(L, slots), ctx->nstreams));
     f->panel_res_rows = panel_res_rows(L);
-    // 8 panels (K = 512 trailing updates) pay off only on large matrices
-    // (cfg4: -2 %; cfg2 at n = 4096: +24 %, the longer in-block chain)
+    // wide outer blocks (16 panels: K = 1024 trailing updates) pay off only on
+    // large matrices (cfg4: -3 % against 4 panels; cfg2 / cfg3: +5 % / +3 %,
+    // the longer in-block chain)
     f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? (N >= 12288 ? 16 : 4) : 2,
                                  FL_MAX_BLOCK_PANELS);
     f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4, 8);
