@@ -643,7 +643,7 @@ int panel_res_rows(int local_nodes) {
 }
 
 // Panels per LU outer block (1..16) / tiles per triangular-solve row block (1..8).
-// Many local nodes (throughput-bound): 4 (16 when N >= 12288), so the trailing
+// Many local nodes (throughput-bound): 4 (16 when N >= 12288; 8 for fewer nodes there), so the trailing
 // updates run with K = 256 (1024; cfg4 LU 11.36 -> 11.21 s, LDL^T 5.48 -> 5.39 s
 // against 8 panels); few (latency-bound: the per-node panel chain sets the step time):
 // 2, so the look-ahead stream has half as many panels to factor per block.
@@ -711,8 +711,10 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     f->panel_res_rows = panel_res_rows(L);
     // wide outer blocks (16 panels: K = 1024 trailing updates) pay off only on
     // large matrices (cfg4: -3 % against 4 panels; cfg2 / cfg3: +5 % / +3 %,
-    // the longer in-block chain)
-    f->lu_panels = block_panels("FEASTLAB_LU_PANELS", L >= 8 ? (N >= 12288 ? 16 : 4) : 2,
+    // the longer in-block chain); at n >= 12288 even 4 local nodes take 8
+    // (cfg4 8-GPU shard 1530 -> 1467 ms against 2 panels)
+    f->lu_panels = block_panels("FEASTLAB_LU_PANELS",
+                                 N >= 12288 ? (L >= 8 ? 16 : 8) : (L >= 8 ? 4 : 2),
                                  FL_MAX_BLOCK_PANELS);
     f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4, 8);
     long long new_facts = 0;

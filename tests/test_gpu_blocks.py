@@ -2,8 +2,8 @@
 FEASTLAB_SOLVE_PANELS: 1..16 LU panels, 1..8 solve tiles of 64): every width, including
 ragged last blocks (N / 64 not a multiple of the width), gives the oracle's
 filter (proj/src/filterop.cpp:62-84) to rounding level. The defaults pick 16
-panels (K = 1024 trailing updates) for >= 8 local nodes of N >= 12288, 4 for
->= 8 local nodes of smaller N, and 2 below."""
+panels (K = 1024 trailing updates) for >= 8 local nodes of N >= 12288 (8 for
+fewer nodes), 4 for >= 8 local nodes of smaller N, and 2 below."""
 import os
 
 import numpy as np
