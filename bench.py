@@ -183,25 +183,45 @@ def build_workload(cfg_index, device):
     return A, vals, c
 
 
-def cpu_sample(c, threads):
+def cpu_sample(c, threads, n=None, node=0):
     """Oracle (restated reference algorithm) on one contour node of the workload:
-    one zI - A LU + m0-RHS solve + accumulation = F_filter / n_c flops."""
+    one zI - A LU + m0-RHS solve + accumulation = F_filter / n_c flops, at
+    order n (default: the workload's), node `node` of the workload's rule."""
     import oracle as O
-    from paper_1605_08771_b200 import configs as CF  # noqa: F401
 
     O.set_threads(threads)
-    n, p = min(c["n"], CPU_SAMPLE_MAX_N), c["m0"]
-    rng = np.random.default_rng(0)
+    n, p = n or c["n"], c["m0"]
+    rng = np.random.default_rng(node)
     M = rng.standard_normal((n, n))
     A = np.asfortranarray(0.5 * (M + M.T) / np.sqrt(n))
     X = np.asfortranarray(rng.standard_normal((n, p)))
     rule = O.build_contour_rule(O.SearchInterval(c["lo"], c["hi"]), c["n_c"])
-    one = O.ContourRule(rule.interval, rule.nodes[:1], rule.weights[:1])
+    k = node % c["n_c"]
+    one = O.ContourRule(rule.interval, rule.nodes[k:k + 1], rule.weights[k:k + 1])
+    del M
     t0 = time.perf_counter()
     O.apply_filter(A, one, X)
     dt = time.perf_counter() - t0
     flops = filter_flops(n, p, 1)
     return flops / dt / 1e9, dt, n
+
+
+def load_configs():
+    """paper_1605_08771_b200/configs.py loaded by path: the seeds and intervals
+    only, without importing the product package (the reference arm must not
+    map libfeastlab_b200.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_fl_configs", os.path.join(ROOT, "paper_1605_08771_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["_fl_configs"] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod
+
+
+# the reference arm's timed steps together stay within this many seconds of
+# host work (a cfg4 node at full order is ~47 s on 16 cores)
+REF_BUDGET_S = 240.0
 
 
 def workload_config(args, c, world):
@@ -215,24 +235,38 @@ def workload_config(args, c, world):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The reference's algorithm on the host cores (oracle/ = proj/src/filterop.cpp
+    restated on OpenBLAS; Eigen is absent, so the reference itself cannot be
+    built). Each timed step is one contour node of the workload (shift, LU,
+    m0-RHS solve, accumulate: F_filter / n_c flops) at the workload's order
+    when K such nodes fit REF_BUDGET_S, else at the largest multiple of 1024
+    that does (said in `sample`); the line also extrapolates the whole
+    application. Nothing from the product package is imported or mapped."""
     if rank != 0:
         return
     import oracle as O  # noqa: F401
-    from paper_1605_08771_b200 import configs as CF
-    import paper_1605_08771_b200 as P
 
-    vals = CF.spectrum(args.config, P.uniform_values)
+    CF = load_configs()
+    vals = CF.spectrum(args.config, O.uniform_fill)
     c = CF.resolved(args.config, vals)
     threads = os.cpu_count() or 1
-    for _ in range(max(args.warmup, 0)):
-        cpu_sample(c, threads)
-    rates = []
-    t_all = 0.0
-    for _ in range(args.steps):
-        r, dt, ns = cpu_sample(c, threads)
+    # warm-up: thread pool and page faults, at a small order (untimed)
+    for w in range(max(args.warmup, 0)):
+        cpu_sample(c, threads, n=min(c["n"], 2048), node=w)
+    # rate probe (untimed) -> order of the timed samples
+    r0, _, _ = cpu_sample(c, threads, n=min(c["n"], 4096), node=0)
+    per_step = REF_BUDGET_S / max(args.steps, 1)
+    n_s = c["n"]
+    while n_s > 1024 and filter_flops(n_s, c["m0"], 1) / (0.9 * r0 * 1e9) > per_step:
+        n_s -= 1024
+    rates, t_all = [], 0.0
+    for k in range(args.steps):
+        r, dt, ns = cpu_sample(c, threads, n=n_s, node=k)
         rates.append(r)
         t_all += dt
     value = float(np.mean(rates))
+    full = "the workload's order" if n_s == c["n"] else f"n={n_s} (workload n={c['n']}; " \
+        f"{args.steps} steps x one node at full order would exceed the {REF_BUDGET_S:.0f} s budget)"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -241,10 +275,15 @@ def run_reference(args, rank, world):
         "config": workload_config(args, c, world),
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"one contour node per step (zI-A LU + m0-RHS solve + "
-                                   f"accumulate) of the workload at n={ns}, m0={c['m0']}, "
-                                   "oracle restatement of proj/src/filterop.cpp on OpenBLAS; "
-                                   "reference (Eigen) unbuildable here"},
+                         "sample": f"one contour node per step (zI-A LU + m0={c['m0']} RHS solve + "
+                                   f"accumulate; node k of the rule at step k) at {full}; oracle "
+                                   "restatement of proj/src/filterop.cpp:9-84 on OpenBLAS "
+                                   "(reference needs Eigen, absent)",
+                         "sample_n": n_s,
+                         "extrapolated_s_per_application": round(
+                             filter_flops(c["n"], c["m0"], c["n_c"]) / (value * 1e9), 1),
+                         "extrapolation": "whole application (n_c nodes at the workload's "
+                                          "order) at the sampled rate: not measured"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -461,7 +500,7 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_cpu_baseline and world == 1:
         try:
             threads = os.cpu_count() or 1
-            rate, dt, ns = cpu_sample(c, threads)
+            rate, dt, ns = cpu_sample(c, threads, n=min(c["n"], CPU_SAMPLE_MAX_N))
             cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
                    "sample": f"one contour node (n={ns}, m0={p}) of the workload: LU + solve + "
                              f"accumulate in {dt:.2f} s, oracle restatement on OpenBLAS",
@@ -470,7 +509,7 @@ def run_b200(args, rank, world, local_rank):
                    "extrapolated_ms_per_step": round(filter_flops(n, p, nc) / (rate * 1e9) * 1e3,
                                                      1)}
             # and on one core (a smaller node keeps it to a few seconds)
-            r1, dt1, n1 = cpu_sample(dict(c, n=min(c["n"], 2048)), 1)
+            r1, dt1, n1 = cpu_sample(c, 1, n=min(c["n"], 2048))
             cpu["one_core"] = {"value": round(r1, 3), "unit": "GFLOP/s", "cores": 1,
                                "sample": f"one contour node (n={n1}, m0={p}) in {dt1:.2f} s"}
         except Exception as e:

@@ -61,6 +61,7 @@ typedef struct fl_ctx fl_ctx;       /* device, stream, NCCL communicator, worksp
 typedef struct fl_matrix fl_matrix; /* device-resident SymmetricMatrix               */
 typedef struct fl_block fl_block;   /* device-resident n x p real block (MatrixXd)    */
 typedef struct fl_filter fl_filter; /* FilterApplier state (rule, factor cache)       */
+typedef struct fl_node fl_node;     /* NodeFactorization: one owned device LU factor  */
 
 /* ------------------------------------------------------------ context */
 int fl_version(void);
@@ -73,6 +74,11 @@ int fl_ctx_create(int device, fl_ctx** out, fl_err* err);
 int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl_ctx** out,
                        fl_err* err);
 int fl_nccl_unique_id(void* out128, fl_err* err);
+/* Test hook: a context that plays rank `rank` of `nranks` for the node
+   sharding only (no communicator): its filters factor and solve the rank's
+   contour nodes and return the rank's partial sum, as a rank of a real clique
+   does just before its all-reduce. Lets one GPU run every shard of a G-GPU job. */
+int fl_ctx_create_virtual(int device, int rank, int nranks, fl_ctx** out, fl_err* err);
 /* contour nodes owned by `rank` of `nranks`: [*k_begin, *k_end), contiguous,
    ascending; the shards of all ranks partition [0, n_c) */
 int fl_node_shard(int n_c, int rank, int nranks, int* k_begin, int* k_end);
@@ -191,6 +197,15 @@ int fl_sym_eig(fl_ctx* ctx, const double* M, int p, int ldm, double* vals, doubl
 /* NodeFactorization(A, z).solve(B) (filterop.cpp:9-32; test hook): interleaved complex */
 int fl_node_solve(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, const double* B, int p,
                   double* W, fl_err* err);
+/* NodeFactorization(A, z, node_index) (filterop.cpp:9-24): factors z I - A once into an
+   owned device factor; FL_SINGULAR_NODE (index = node_index) when a U diagonal entry is
+   zero or non-finite. The factor lives until fl_node_destroy. */
+int fl_node_create(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, int node_index,
+                   fl_node** out, fl_err* err);
+/* NodeFactorization::solve (filterop.cpp:26-32): W = (z I - A)^{-1} B against the owned
+   factor, B and W host n x p interleaved complex (column-major); no refactorisation */
+int fl_node_factor_solve(fl_node* node, const double* B, int p, double* W, fl_err* err);
+int fl_node_destroy(fl_node* node);
 
 /* ------------------------------------------------------------ host-level entry points
    (the drop-in C++ layer, exported for foreign callers) */

@@ -48,6 +48,7 @@ _SIGS = {
     "fl_ctx_create": (_I, [_I, _PP, _P]),
     "fl_ctx_create_nccl": (_I, [_I, _P, _I, _I, _PP, _P]),
     "fl_nccl_unique_id": (_I, [_P, _P]),
+    "fl_ctx_create_virtual": (_I, [_I, _I, _I, _PP, _P]),
     "fl_node_shard": (_I, [_I, _I, _I, _P, _P]),
     "fl_ctx_destroy": (_I, [_P]),
     "fl_ctx_sync": (_I, [_P, _P]),
@@ -91,6 +92,9 @@ _SIGS = {
     "fl_block_rank": (_I, [_P, _P, _D, _P, _P]),
     "fl_sym_eig": (_I, [_P, _P, _I, _I, _P, _P, _I, _P]),
     "fl_node_solve": (_I, [_P, _P, _D, _D, _P, _I, _P, _P]),
+    "fl_node_create": (_I, [_P, _P, _D, _D, _I, _PP, _P]),
+    "fl_node_factor_solve": (_I, [_P, _P, _I, _P, _P]),
+    "fl_node_destroy": (_I, [_P]),
     "fl_solve": (_I, [_P, _I, _P, _I, _I, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                       _P, _P]),
     "fl_gauss_legendre": (_I, [_I, _P, _P, _P]),

@@ -202,11 +202,14 @@ struct fl_filter {
         long ldx, ldy;
         int p, slots, ns, zmode, reduction, factorization;
         int phase;  // 0: factor + solve (no cache); cache: 1 factor + solve, 2 solve only
+        int lu_panels, solve_panels, panel_res_rows;  // blocking (environment-tunable)
         bool operator==(const GraphKey& o) const {
             return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
                    ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns &&
                    zmode == o.zmode && reduction == o.reduction &&
-                   factorization == o.factorization && phase == o.phase;
+                   factorization == o.factorization && phase == o.phase &&
+                   lu_panels == o.lu_panels && solve_panels == o.solve_panels &&
+                   panel_res_rows == o.panel_res_rows;
         }
     };
     GraphKey gkey{}, gseen{};
@@ -291,6 +294,7 @@ void sync(fl_ctx* ctx) {
         }
         CK(e);
     }
+    CK(cudaGetLastError());  // a refused launch (bad configuration) raises here
     if (!ctx->pending.empty()) resolve_pending(ctx);
 }
 
@@ -384,16 +388,11 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     const int NPB = f->lu_panels;  // panels per outer block (2: 128 columns, 4: 256)
     int* tabs[FL_MAX_BLOCK_PANELS];
     for (int j = 0; j < NPB; ++j) tabs[j] = ptab + (long)(j * f->fac_slots) * (4 * T + 1);
-    static const int dbg_skip = [] {  // timing experiments only: results are wrong
-        const char* e = std::getenv("FEASTLAB_DEBUG_SKIP");
-        return e ? std::atoi(e) : 0;
-    }();
     auto panel = [&](int k, int* tab) {
         Prof pr(ctx, P_PANEL, 0.0, 1, sp);  // also writes L_kk^{-1} into Inv
-        if (!(dbg_skip & 1)) launch_panel(F, N, k, ipiv, tab, Inv, G, sp, f->panel_res_rows);
+        launch_panel(F, N, k, ipiv, tab, Inv, G, sp, f->panel_res_rows);
     };
     auto swaps = [&](const int* tab, int a0, int a1, int b0, int b1, cudaStream_t s) {
-        if (dbg_skip & 4) return;
         Prof pr(ctx, P_LASWP, 0.0, 1, s);
         launch_laswp(F, a0, a1, b0, b1, tab, G, s);
     };
@@ -653,6 +652,14 @@ int block_panels(const char* env, int dflt, int most) {
     return std::max(1, std::min(most, v));
 }
 
+// Serialises the free-memory read and the allocation of factor slots per
+// device: concurrent solves on one GPU (solve_concurrently, per_device > 1)
+// each see the memory the others already took.
+std::mutex& device_alloc_mutex(int device) {
+    static std::mutex mu[64];
+    return mu[device & 63];
+}
+
 size_t free_bytes() {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -675,6 +682,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->w_P = P;
     }
     // factor slots
+    std::unique_lock<std::mutex> alloc_lk(device_alloc_mutex(ctx->device));
     int slots;
     if (f->cache) {
         slots = L;
@@ -699,6 +707,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->fac_slots = slots;
         std::fill(f->factored.begin(), f->factored.end(), 0);
     }
+    alloc_lk.unlock();
     if (f->fac_mode != ctx->factorization) {  // cached factors of the other kind
         std::fill(f->factored.begin(), f->factored.end(), 0);
         f->fac_mode = ctx->factorization;
@@ -721,8 +730,15 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // everything below is stream work only (no host synchronisation), so a
     // non-cache application is one CUDA graph: ~2.8k launches on 9 streams
     // replayed with one cudaGraphLaunch instead of host-paced launches
+    bool needs_factor = !f->cache;
+    if (f->cache)
+        for (char d : f->factored) needs_factor |= !d;
     auto enqueue = [&] {
-        CK(cudaMemsetAsync(f->bad.p, 0x7f, sizeof(int), ctx->stream));  // sentinel 0x7f7f7f7f
+        // sentinel 0x7f7f7f7f = no singular node. Only an application that
+        // factors resets it: a solve-only application (cached factors) keeps
+        // the verdict of the application that built them, so a singular node
+        // is raised even when the caller applies again before syncing
+        if (needs_factor) CK(cudaMemsetAsync(f->bad.p, 0x7f, sizeof(int), ctx->stream));
         CK(cudaEventRecord(ctx->fork, ctx->stream));
         for (int j = 0; j < ns; ++j) CK(cudaStreamWaitEvent(ctx->aux[j], ctx->fork, 0));
         if (f->cache) {
@@ -732,8 +748,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
                 int g = c0;
                 while (g < c1) {
                     if (f->factored[g]) { ++g; continue; }
-                    int e = g;
-                    while (e < c1 && !f->factored[e]) ++e;
+                    int e = g;  // a run of unfactored nodes, at most 16 per batch
+                    while (e < c1 && e - g < 16 && !f->factored[e]) ++e;
                     factor_group(f, g, e - g, g, ctx->aux[j], ctx->paux[j], ctx->ev_panel[j],
                                  ctx->ev_next[j]);
                     for (int k = g; k < e; ++k) f->factored[k] = 1;
@@ -761,13 +777,21 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             CK(cudaEventRecord(ctx->join[j], ctx->aux[j]));
             CK(cudaStreamWaitEvent(ctx->stream, ctx->join[j], 0));
         }
-        // ordered accumulation over the local nodes
-        NodeShifts w{};
-        for (int b = 0; b < L; ++b) {
-            w.zr[b] = f->wr[f->kb + b];
-            w.zi[b] = f->wi[f->kb + b];
-        }
+        // ordered accumulation over the local nodes, in launches of at most
+        // kMaxNodes weights (a later launch continues the same ascending sum
+        // from Y: the association is unchanged)
+        auto weights = [&](int b0, int cnt) {
+            NodeShifts w{};
+            for (int b = 0; b < cnt; ++b) {
+                w.zr[b] = f->wr[f->kb + b0 + b];
+                w.zi[b] = f->wi[f->kb + b0 + b];
+            }
+            return w;
+        };
         ZBatch W{f->w_re.d(), f->w_im.d(), N, f->w_stride};
+        auto wslice = [&](int b0) {
+            return ZBatch{W.re + b0 * W.stride, W.im + b0 * W.stride, W.ld, W.stride};
+        };
         if (ctx->comm && ctx->reduction == FL_REDUCE_ORDERED) {
             // every rank's terms at slot rank * Lmax + local index; all-gather;
             // ascending global-k sum on every rank (bitwise G-invariant)
@@ -777,27 +801,38 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
             const long ts = (long)N * P;
             double* T = scratch(f->terms, (size_t)std::max(Lmax, 1) * ts);
             double* Tall = scratch(f->terms_all, (size_t)G * std::max(Lmax, 1) * ts);
-            NodeSlots sl{};
+            std::vector<int> slot(f->nc);
             for (int r = 0; r < G; ++r) {
                 int b0 = 0, b1 = 0;
                 fl_node_shard(f->nc, r, G, &b0, &b1);
-                for (int k = b0; k < b1; ++k) sl.slot[k] = r * Lmax + (k - b0);
+                for (int k = b0; k < b1; ++k) slot[k] = r * Lmax + (k - b0);
             }
-            {
-                Prof pr(ctx, P_ACCUM, 24.0 * L * N * P);
-                launch_node_terms(W, N, P, w, L, T, ts, ctx->stream);
+            for (int b0 = 0; b0 < L; b0 += kMaxNodes) {
+                const int cnt = std::min(kMaxNodes, L - b0);
+                Prof pr(ctx, P_ACCUM, 24.0 * cnt * N * P);
+                launch_node_terms(wslice(b0), N, P, weights(b0, cnt), cnt, T + b0 * ts, ts,
+                                  ctx->stream);
             }
             Prof pr(ctx, P_ALLREDUCE, 8.0 * G * Lmax * ts, 1);
             nccl_check(ncclAllGather(T, Tall, (size_t)Lmax * ts, ncclFloat64, ctx->comm,
                                      ctx->stream),
                        "ncclAllGather(node terms)");
-            launch_ordered_sum(Tall, ts, sl, f->nc, N, P, Y, ldy, ctx->stream);
+            for (int k0 = 0; k0 < f->nc; k0 += kMaxNodes) {
+                NodeSlots sl{};
+                const int cnt = std::min(kMaxNodes, f->nc - k0);
+                for (int k = 0; k < cnt; ++k) sl.slot[k] = slot[k0 + k];
+                launch_ordered_sum(Tall, ts, sl, cnt, N, P, Y, ldy, k0 > 0, ctx->stream);
+            }
             nccl_check(ncclAllReduce(f->bad.p, f->bad.p, 1, ncclInt32, ncclMin, ctx->comm,
                                      ctx->stream),
                        "ncclAllReduce(bad node)");
         } else if (L > 0) {
-            Prof pr(ctx, P_ACCUM, (16.0 * L + 8.0) * N * P);
-            launch_accumulate(W, N, P, w, L, Y, ldy, false, ctx->stream);
+            for (int b0 = 0; b0 < L; b0 += kMaxNodes) {
+                const int cnt = std::min(kMaxNodes, L - b0);
+                Prof pr(ctx, P_ACCUM, (16.0 * cnt + (b0 > 0 ? 16.0 : 8.0)) * N * P);
+                launch_accumulate(wslice(b0), N, P, weights(b0, cnt), cnt, Y, ldy, b0 > 0,
+                                  ctx->stream);
+            }
         } else {
             CK(cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)ldy * P, ctx->stream));
         }
@@ -823,12 +858,10 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     // than an eager application saves). Cached factorizations: the factoring
     // application is captured too (launched once, phase 1), the solve-only
     // ones are replayed (phase 2).
-    bool needs_factor = false;
-    if (f->cache)
-        for (char d : f->factored) needs_factor |= !d;
     const int phase = f->cache ? (needs_factor ? 1 : 2) : 0;
     const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
-                                  zgemm_mode(), ctx->reduction, ctx->factorization, phase};
+                                  zgemm_mode(), ctx->reduction, ctx->factorization, phase,
+                                  f->lu_panels, f->solve_panels, f->panel_res_rows};
     const bool graphable = !ctx->prof.on && graphs_enabled();
     const bool big = N >= 2048;
     if (graphable && f->gexec && f->gkey == key && phase != 1) {
@@ -846,6 +879,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         cudaGraph_t graph = nullptr;
         try {
             enqueue();
+            launch_check(cudaGetLastError(), "filter application (capture)");
         } catch (...) {
             cudaStreamEndCapture(ctx->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -866,6 +900,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     } else {
         f->gseen = key;
         enqueue();
+        launch_check(cudaGetLastError(), "filter application");
     }
     // the singular-node verdict travels to pinned memory behind the work; the
     // host does not wait for it here (a host round trip per application
@@ -1154,6 +1189,8 @@ int guarded(fl_err* err, F&& body) {
         return FL_OK;
     } catch (const Fail& f) {
         return report(err, f);
+    } catch (const LaunchError& e) {
+        return report(err, Fail{FL_CUDA, e.what()});
     } catch (const std::bad_alloc&) {
         return report(err, Fail{FL_OOM, "host allocation failed"});
     } catch (const std::exception& e) {
@@ -1230,6 +1267,12 @@ int fl_ctx_create_nccl(int device, const void* nccl_id, int rank, int nranks, fl
     if (nranks < 1 || rank < 0 || rank >= nranks || nccl_id == nullptr)
         return report(err, Fail{FL_INVALID_ARGUMENT, "bad rank/nranks or missing NCCL id"});
     return ctx_create_impl(device, nccl_id, rank, nranks, out, err);
+}
+
+int fl_ctx_create_virtual(int device, int rank, int nranks, fl_ctx** out, fl_err* err) {
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return report(err, Fail{FL_INVALID_ARGUMENT, "bad rank/nranks"});
+    return ctx_create_impl(device, nullptr, rank, nranks, out, err);
 }
 
 int fl_nccl_unique_id(void* out128, fl_err* err) {
@@ -1550,8 +1593,7 @@ int fl_block_copy(fl_block* dst, const fl_block* src, fl_err* err) {
 int fl_filter_create(fl_ctx* ctx, const fl_matrix* A, int n_c, const double* zr, const double* zi,
                      const double* wr, const double* wi, int cache, fl_filter** out, fl_err* err) {
     return guarded(err, [&] {
-        if (n_c < 1 || n_c > kMaxNodes)
-            throw Fail{FL_INVALID_ARGUMENT, "fl_filter_create: need 1 <= n_c <= 64"};
+        if (n_c < 1) throw Fail{FL_INVALID_ARGUMENT, "fl_filter_create: need n_c >= 1"};
         std::unique_ptr<fl_filter> f(new fl_filter());
         f->ctx = ctx;
         f->A = A;
@@ -1718,56 +1760,146 @@ int fl_sym_eig(fl_ctx* ctx, const double* M, int p, int ldm, double* vals, doubl
     });
 }
 
+}  // extern "C"
+
+struct fl_node {
+    fl_ctx* ctx = nullptr;
+    int node_index = -1;
+    std::unique_ptr<fl_filter> f;
+};
+
+namespace {
+
+// A one-node cached filter (weight 1) holding the factor of z I - A.
+std::unique_ptr<fl_filter> node_filter(fl_ctx* ctx, const fl_matrix* A, double zr, double zi) {
+    std::unique_ptr<fl_filter> f(new fl_filter());
+    f->ctx = ctx;
+    f->A = A;
+    f->nc = 1;
+    f->zr = {zr};
+    f->zi = {zi};
+    f->wr = {1.0};
+    f->wi = {0.0};
+    f->cache = true;
+    f->kb = 0;
+    f->ke = 1;
+    f->factored.assign(1, 0);
+    return f;
+}
+
+// W = S^{-1} (Br + i Bi) = S^{-1} Br + i S^{-1} Bi, both halves through the
+// real-RHS path of the (cached) factor; B, W host interleaved complex n x p.
+void node_solve_impl(fl_filter* f, const double* B, int p, double* W) {
+    fl_ctx* ctx = f->ctx;
+    const int n = f->A->n, N = f->A->N;
+    const int P = round_up(2 * p, FL_TILE);
+    DBuf X;
+    X.ensure(sizeof(double) * (size_t)N * P);
+    CK(cudaMemsetAsync(X.p, 0, sizeof(double) * (size_t)N * P, ctx->stream));
+    std::vector<double> h((size_t)n * 2 * p);
+    for (int c = 0; c < p; ++c)
+        for (int i = 0; i < n; ++i) {
+            h[(size_t)c * n + i] = B[2 * ((size_t)c * n + i)];
+            h[(size_t)(p + c) * n + i] = B[2 * ((size_t)c * n + i) + 1];
+        }
+    copy_in(ctx, X.d(), N, n, h.data(), n, 2 * p, FL_HOST);
+    DBuf Y;
+    Y.ensure(sizeof(double) * (size_t)N * P);
+    // weight 1: Y = Re(W) for the real RHS; fetch the W planes directly
+    filter_apply_dev(f, X.d(), N, 2 * p, Y.d(), N, nullptr, nullptr);
+    std::vector<double> wr((size_t)N * P), wi((size_t)N * P);
+    CK(cudaMemcpyAsync(wr.data(), f->w_re.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(wi.data(), f->w_im.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    sync(ctx);
+    for (int c = 0; c < p; ++c)
+        for (int i = 0; i < n; ++i) {
+            const double ar = wr[(size_t)c * N + i], ai = wi[(size_t)c * N + i];
+            const double br = wr[(size_t)(p + c) * N + i], bi = wi[(size_t)(p + c) * N + i];
+            W[2 * ((size_t)c * n + i)] = ar - bi;
+            W[2 * ((size_t)c * n + i) + 1] = ai + br;
+        }
+}
+
+void node_release(fl_filter* f) {
+    auto& pend = f->ctx->pending;
+    pend.erase(std::remove(pend.begin(), pend.end(), f), pend.end());
+}
+
+}  // namespace
+
+extern "C" {
+
 int fl_node_solve(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, const double* B, int p,
                   double* W, fl_err* err) {
     return guarded(err, [&] {
         if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "node solve: p must be >= 1"};
         CtxLock lk(ctx);
-        // factor one node, solve with a complex RHS: W = S^{-1} (Br + i Bi)
-        // = S^{-1} Br + i S^{-1} Bi, each through the real-RHS path
-        const int n = A->n, N = A->N;
-        fl_filter f;
-        f.ctx = ctx;
-        f.A = A;
-        f.nc = 1;
-        f.zr = {zr};
-        f.zi = {zi};
-        f.wr = {1.0};
-        f.wi = {0.0};
-        f.cache = true;
-        f.kb = 0;
-        f.ke = 1;
-        f.factored.assign(1, 0);
-        const int P = round_up(2 * p, FL_TILE);
-        DBuf X;
-        X.ensure(sizeof(double) * (size_t)N * P);
-        CK(cudaMemsetAsync(X.p, 0, sizeof(double) * (size_t)N * P, ctx->stream));
-        std::vector<double> h((size_t)n * 2 * p);
-        for (int c = 0; c < p; ++c)
-            for (int i = 0; i < n; ++i) {
-                h[(size_t)c * n + i] = B[2 * ((size_t)c * n + i)];
-                h[(size_t)(p + c) * n + i] = B[2 * ((size_t)c * n + i) + 1];
-            }
-        copy_in(ctx, X.d(), N, n, h.data(), n, 2 * p, FL_HOST);
-        DBuf Y;
-        Y.ensure(sizeof(double) * (size_t)N * P);
-        // weight 1: Y = Re(W) for the real RHS; fetch W planes directly
-        filter_apply_dev(&f, X.d(), N, 2 * p, Y.d(), N, nullptr, nullptr);
-        std::vector<double> wr((size_t)N * P), wi((size_t)N * P);
-        CK(cudaMemcpyAsync(wr.data(), f.w_re.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CK(cudaMemcpyAsync(wi.data(), f.w_im.p, sizeof(double) * (size_t)N * P, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        sync(ctx);
-        for (int c = 0; c < p; ++c)
-            for (int i = 0; i < n; ++i) {
-                // (S^{-1} Br) + i (S^{-1} Bi)
-                const double ar = wr[(size_t)c * N + i], ai = wi[(size_t)c * N + i];
-                const double br = wr[(size_t)(p + c) * N + i], bi = wi[(size_t)(p + c) * N + i];
-                W[2 * ((size_t)c * n + i)] = ar - bi;
-                W[2 * ((size_t)c * n + i) + 1] = ai + br;
-            }
+        std::unique_ptr<fl_filter> f = node_filter(ctx, A, zr, zi);
+        try {
+            node_solve_impl(f.get(), B, p, W);
+        } catch (...) {
+            node_release(f.get());
+            throw;
+        }
+        node_release(f.get());
     });
+}
+
+int fl_node_create(fl_ctx* ctx, const fl_matrix* A, double zr, double zi, int node_index,
+                   fl_node** out, fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        std::unique_ptr<fl_node> nd(new fl_node());
+        nd->ctx = ctx;
+        nd->node_index = node_index;
+        nd->f = node_filter(ctx, A, zr, zi);
+        // factor now (a one-column solve rides along), so a singular shift
+        // raises here, as the reference constructor does (filterop.cpp:13-23)
+        std::vector<double> b(2 * (size_t)A->n, 0.0), w(2 * (size_t)A->n);
+        try {
+            node_solve_impl(nd->f.get(), b.data(), 1, w.data());
+        } catch (Fail& e) {
+            node_release(nd->f.get());
+            if (e.code == FL_SINGULAR_NODE) {
+                char buf[256];
+                std::snprintf(buf, sizeof(buf),
+                              "factorize_node: singular factorization at node %d (z = %f+%fi)",
+                              node_index, zr, zi);
+                e.msg = buf;
+                e.index = node_index;
+            }
+            throw;
+        } catch (...) {
+            node_release(nd->f.get());
+            throw;
+        }
+        ctx_retain(ctx);
+        *out = nd.release();
+    });
+}
+
+int fl_node_factor_solve(fl_node* node, const double* B, int p, double* W, fl_err* err) {
+    return guarded(err, [&] {
+        if (p < 1) throw Fail{FL_INVALID_ARGUMENT, "node solve: p must be >= 1"};
+        CtxLock lk(node->ctx);
+        node_solve_impl(node->f.get(), B, p, W);
+    });
+}
+
+int fl_node_destroy(fl_node* node) {
+    if (node) {
+        fl_ctx* ctx = node->ctx;
+        {
+            CtxLock lk(ctx);
+            cudaStreamSynchronize(ctx->stream);
+            node_release(node->f.get());
+            delete node;
+        }
+        ctx_release(ctx);
+    }
+    return FL_OK;
 }
 
 }  // extern "C"

@@ -31,25 +31,27 @@ void split_rule(const ContourRule& rule, std::vector<double>& zr, std::vector<do
 
 NodeFactorization::NodeFactorization(const SymmetricMatrix& A, std::complex<double> z,
                                      int node_index)
-    : A_(&A), z_(z), node_index_(node_index) {
-    // factor once up front so a singular shift throws here, as in the reference
-    MatrixXcd probe(A.dim(), 1);
-    (void)solve(probe);
-}
-
-MatrixXcd NodeFactorization::solve(const MatrixXcd& X) const {
+    : z_(z), node_index_(node_index) {
+    // factor once up front into an owned device factor; a singular shift
+    // throws here with the reference's message (filterop.cpp:13-23)
     fl_ctx* ctx = current_context();
-    DeviceMatrix dA(ctx, A_->mat());
-    MatrixXcd W(X.rows(), X.cols());
+    fl_node* nd = nullptr;
     fl_err err{};
-    const int st = fl_node_solve(ctx, dA.get(), z_.real(), z_.imag(),
-                                 reinterpret_cast<const double*>(X.data()), X.cols(),
-                                 reinterpret_cast<double*>(W.data()), &err);
+    const int st = fl_node_create(ctx, A.device(ctx).get(), z.real(), z.imag(), node_index, &nd, &err);
     if (st == FL_SINGULAR_NODE)
         throw std::runtime_error("factorize_node: singular factorization at node " +
                                  std::to_string(node_index_) + " (z = " + std::to_string(z_.real()) +
                                  "+" + std::to_string(z_.imag()) + "i)");
     check(st, err);
+    node_.reset(nd, [](fl_node* p) { fl_node_destroy(p); });
+}
+
+MatrixXcd NodeFactorization::solve(const MatrixXcd& X) const {
+    MatrixXcd W(X.rows(), X.cols());
+    fl_err err{};
+    check(fl_node_factor_solve(node_.get(), reinterpret_cast<const double*>(X.data()), X.cols(),
+                               reinterpret_cast<double*>(W.data()), &err),
+          err);
     return W;
 }
 
@@ -74,7 +76,7 @@ FilterApplier::FilterApplier(const SymmetricMatrix& A, const ContourRule& rule,
                              bool cache_factorizations)
     : A_(A), rule_(rule), cache_(cache_factorizations) {
     fl_ctx* ctx = current_context();
-    dA_ = std::make_unique<DeviceMatrix>(ctx, A.mat());
+    dA_ = &A.device(ctx);
     std::vector<double> zr, zi, wr, wi;
     split_rule(rule, zr, zi, wr, wi);
     fl_err err{};

@@ -2,8 +2,12 @@
 // asymmetry check, exact symmetrisation (M + M^T)/2.
 #include "feastlab/matmodel.hpp"
 
+#include "feastlab/device.hpp"
+
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -49,6 +53,23 @@ void SymmetricMatrix::init(const double* e, int n, long lde, double sym_tol) {
         throw std::invalid_argument("SymmetricMatrix: input not symmetric (max |A - A^T| = " +
                                     std::to_string(asym) + ")");
     mat_ = std::move(out);
+    dev_ = std::make_shared<DeviceCache>();
+}
+
+// One device copy per context, uploaded on first use (contexts are
+// per-thread / per-GPU, so concurrent solves each get their own).
+struct SymmetricMatrix::DeviceCache {
+    std::mutex mu;
+    std::map<fl_ctx*, std::unique_ptr<DeviceMatrix>> copies;
+};
+
+const DeviceMatrix& SymmetricMatrix::device(fl_ctx* ctx) const {
+    // dev_ is created at construction time (see init) so the const accessor
+    // never races on the pointer itself
+    std::lock_guard<std::mutex> lk(dev_->mu);
+    auto& slot = dev_->copies[ctx];
+    if (!slot) slot = std::make_unique<DeviceMatrix>(ctx, mat_);
+    return *slot;
 }
 
 }  // namespace feastlab

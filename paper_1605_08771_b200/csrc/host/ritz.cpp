@@ -36,7 +36,7 @@ RitzSet rayleigh_ritz(const SymmetricMatrix& A, const MatrixXd& X, const SearchI
     const int p = X.cols();
     if (p < 1) throw std::invalid_argument("rayleigh_ritz: empty block");
     fl_ctx* ctx = current_context();
-    DeviceMatrix dA(ctx, A.mat());
+    const DeviceMatrix& dA = A.device(ctx);
     DeviceBlock dX(ctx, X.rows(), p), dV(ctx, X.rows(), p);
     dX.set(X);
     RitzSet out;
@@ -54,7 +54,7 @@ RitzSet rayleigh_ritz(const SymmetricMatrix& A, const MatrixXd& X, const SearchI
 
 MatrixXd compute_residual_block(const SymmetricMatrix& A, const RitzSet& ritz) {
     fl_ctx* ctx = current_context();
-    DeviceMatrix dA(ctx, A.mat());
+    const DeviceMatrix& dA = A.device(ctx);
     DeviceBlock dV(ctx, ritz.vectors.rows(), std::max(1, ritz.vectors.cols()));
     DeviceBlock dR(ctx, ritz.vectors.rows(), std::max(1, ritz.vectors.cols()));
     dV.set(ritz.vectors);

@@ -3,10 +3,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdexcept>
+#include <string>
+
 namespace fl {
+
+// A kernel launch the runtime refused (bad configuration, missing attribute):
+// the C ABI reports it as FL_CUDA.
+struct LaunchError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+inline void launch_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw LaunchError(std::string(what) + ": " + cudaGetErrorString(e));
+}
 
 // Opt a kernel into > 48 KB dynamic shared memory once per (kernel, device).
 void ensure_smem(const void* func, size_t bytes);
+// Set a function attribute once per (kernel, device, attribute): the settings
+// are per device, so a process driving several GPUs must set them on each.
+void ensure_attr(const void* func, cudaFuncAttribute attr, int value);
 
 // Real C = alpha op(A) op(B) + beta C. M, N multiples of 64; K multiple of 16.
 struct DGemm {
@@ -50,6 +65,8 @@ struct ZBatch {
     long stride;
 };
 
+// nodes per launch of the node-batched kernels (a filter has any number of
+// nodes: the orchestration launches them in groups of at most kMaxNodes)
 constexpr int kMaxNodes = 64;
 struct NodeShifts {
     double zr[kMaxNodes];
@@ -94,8 +111,9 @@ struct NodeSlots {
 };
 void launch_node_terms(ZBatch W, int N, int P, const NodeShifts& w, int batch, double* T,
                        long tstride, cudaStream_t s);
+// Y [+]= sum_k T[slot[k]] for the nc (<= kMaxNodes) slots given, ascending
 void launch_ordered_sum(const double* T, long tstride, const NodeSlots& sl, int nc, int N, int P,
-                        double* Y, long ldy, cudaStream_t s);
+                        double* Y, long ldy, bool add_to_Y, cudaStream_t s);
 // Complex-symmetric LDL^T without interchanges (ldlt.cu): factor the 64x64
 // diagonal block at (k0, k0) of every node (lower triangle read), write L_kk,
 // D_k, U_kk = D_k L_kk^T in place, L_kk^{-1} into Inv block k0/64 and L_kk^{-T}

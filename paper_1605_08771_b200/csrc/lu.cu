@@ -30,9 +30,23 @@ void ensure_smem(const void* func, size_t bytes) {
     std::lock_guard<std::mutex> lk(mu);
     size_t& have = done[{func, dev}];
     if (bytes > have) {
-        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        launch_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                     "cudaFuncSetAttribute(max dynamic shared memory)");
         have = bytes;
     }
+}
+
+void ensure_attr(const void* func, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::map<std::pair<std::pair<const void*, int>, int>, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(std::make_pair(func, dev), (int)attr);
+    auto it = done.find(key);
+    if (it != done.end() && it->second == value) return;
+    launch_check(cudaFuncSetAttribute(func, attr, value), "cudaFuncSetAttribute");
+    done[key] = value;
 }
 
 // ------------------------------------------------------------------ shift
@@ -354,12 +368,12 @@ __global__ void node_terms_kernel(ZBatch W, int N, int P, NodeShifts w, int batc
 }
 
 __global__ void ordered_sum_kernel(const double* __restrict__ T, long tstride, NodeSlots sl, int nc,
-                                   int N, int P, double* Y, long ldy) {
+                                   int N, int P, double* Y, long ldy, bool add) {
     const long total = (long)N * P;
     for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (long)gridDim.x * blockDim.x) {
         const long c = e / N, r = e - c * N;
-        double y = 0.0;
+        double y = add ? Y[c * ldy + r] : 0.0;
         for (int k = 0; k < nc; ++k) y = __dadd_rn(y, T[sl.slot[k] * tstride + e]);
         Y[c * ldy + r] = y;
     }
@@ -373,9 +387,9 @@ void launch_node_terms(ZBatch W, int N, int P, const NodeShifts& w, int batch, d
 }
 
 void launch_ordered_sum(const double* T, long tstride, const NodeSlots& sl, int nc, int N, int P,
-                        double* Y, long ldy, cudaStream_t s) {
+                        double* Y, long ldy, bool add_to_Y, cudaStream_t s) {
     if (P <= 0) return;
-    ordered_sum_kernel<<<148 * 4, 256, 0, s>>>(T, tstride, sl, nc, N, P, Y, ldy);
+    ordered_sum_kernel<<<148 * 4, 256, 0, s>>>(T, tstride, sl, nc, N, P, Y, ldy, add_to_Y);
 }
 
 // ------------------------------------------------------------------ singularity check

@@ -619,12 +619,9 @@ static void launch_res(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv
     static_assert(2 * RPW * (RPW + 1) * sizeof(double) <= sizeof(double2) * NSLOT * RW * RNT,
                   "L_kk staging must fit the slot storage");
     auto kern = panel_res_kernel<CL>;
-    static bool init = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        return true;
-    }();
-    (void)init;
+    // per device (a process may drive several GPUs: solve_concurrently)
+    ensure_smem((const void*)kern, sm);
+    if (CL > 8) ensure_attr((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL, batch);
     cfg.blockDim = dim3(RNT);
@@ -637,7 +634,7 @@ static void launch_res(ZBatch F, int N, int k0, int* ipiv, int* ptab, ZBatch Inv
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, F, N, k0, ipiv, ptab, Inv);
+    launch_check(cudaLaunchKernelEx(&cfg, kern, F, N, k0, ipiv, ptab, Inv), "panel_res launch");
 }
 
 // Resident panel for rows = N - k0 <= 4096: the smallest cluster whose CTAs

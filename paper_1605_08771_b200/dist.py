@@ -43,11 +43,18 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+def rendezvous_nccl_id(rank: int) -> bytes:
+    """Rank 0 makes the ncclUniqueId (fl_nccl_unique_id); every rank receives it
+    over the torch.distributed rendezvous group."""
+    from .feastlab import Context
+    uid = Context.nccl_unique_id() if rank == 0 else None
+    return broadcast_bytes(uid, 128, 0)
+
+
 def make_context(rank: int, world: int, local_rank: int):
     """fl_ctx for this rank: NCCL clique over all ranks when world > 1."""
     from .feastlab import Context
     if world == 1:
         return Context(local_rank)
-    uid = Context.nccl_unique_id() if rank == 0 else None
-    uid = broadcast_bytes(uid, 128, 0)
+    uid = rendezvous_nccl_id(rank)
     return Context(local_rank, nccl_id=uid, rank=rank, nranks=world)

@@ -98,9 +98,13 @@ class Context:
     """fl_ctx: one GPU (and optionally one rank of an NCCL clique)."""
 
     def __init__(self, device: int = 0, *, nccl_id: bytes | None = None, rank: int = 0,
-                 nranks: int = 1):
+                 nranks: int = 1, virtual: bool = False):
+        """virtual=True: rank `rank` of `nranks` for the node sharding only, no
+        communicator (fl_ctx_create_virtual; filters return the rank's partial sum)."""
         h = C.c_void_p()
-        if nccl_id is not None:
+        if virtual:
+            _call(L.lib().fl_ctx_create_virtual, device, rank, nranks, C.byref(h))
+        elif nccl_id is not None:
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             _call(L.lib().fl_ctx_create_nccl, device, buf, rank, nranks, C.byref(h))
         else:
@@ -396,14 +400,21 @@ class SolveAccounting:
 
 
 class NodeFactorization:
-    """NodeFactorization(A, z) (proj/src/filterop.cpp:9-32): complex LU of z I - A."""
+    """NodeFactorization(A, z) (proj/src/filterop.cpp:9-32): complex LU of z I - A,
+    factored once at construction into an owned device factor (fl_node);
+    solve() runs only the triangular solves against it."""
 
     def __init__(self, A, z: complex, node_index: int = -1, ctx: Context | None = None):
         self.ctx = ctx or default_context()
         self._dA = DeviceMatrix(A, self.ctx)
         self.z = complex(z)
         self.node_index = node_index
-        self.solve(np.zeros((self._dA.n, 1)))  # singular shifts throw at construction
+        self.handle = None
+        h = C.c_void_p()
+        # singular shifts throw here, as the reference constructor does
+        _call(L.lib().fl_node_create, self.ctx.handle, self._dA.handle, self.z.real, self.z.imag,
+              int(node_index), C.byref(h))
+        self.handle = h
 
     def shift(self):
         return self.z
@@ -416,9 +427,15 @@ class NodeFactorization:
         if n != self._dA.n:
             raise InvalidArgument("NodeFactorization::solve: dimension mismatch")
         W = np.zeros((n, p), dtype=np.complex128, order="F")
-        _call(L.lib().fl_node_solve, self.ctx.handle, self._dA.handle, self.z.real, self.z.imag,
-              _ptr(B), p, _ptr(W))
+        _call(L.lib().fl_node_factor_solve, self.handle, _ptr(B), p, _ptr(W))
         return W
+
+    def __del__(self):
+        try:
+            if self.handle:
+                L.lib().fl_node_destroy(self.handle)
+        except Exception:
+            pass
 
 
 def factorize_node(A, z: complex) -> NodeFactorization:

@@ -21,6 +21,14 @@ def _free_port():
 
 
 def _worker(rank, world, port, out):
+    """The product's host-side multi-rank logic on `world` CPU ranks: the NCCL
+    id rendezvous of dist.make_context (fl_nccl_unique_id on rank 0, broadcast
+    over gloo), the contour rule built by the product's host code (bitwise the
+    same on every rank), the node shard of fl_node_shard, the max-over-ranks
+    timing helper, and the loud failure of the data-path context without a GPU.
+    Each rank's shard of the filter is computed by the oracle (the checker: the
+    product's kernels need the B200) and the sum all-reduced, reproducing the
+    single-process filter."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -28,26 +36,42 @@ def _worker(rank, world, port, out):
         import torch
 
         import oracle as O
+        import paper_1605_08771_b200 as P
         from paper_1605_08771_b200 import dist as D
-        # rendezvous helpers
-        uid = bytes(range(128)) if rank == 0 else None
-        got = D.broadcast_bytes(uid, 128, 0)
-        assert got == bytes(range(128))
+        # NCCL id rendezvous (dist.make_context): identical 128 bytes on every rank
+        uid = D.rendezvous_nccl_id(rank)
+        ids = [torch.zeros(128, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(ids, torch.tensor(list(uid), dtype=torch.uint8))
+        assert all(torch.equal(ids[0], t) for t in ids) and any(uid)
         assert D.max_over_ranks(float(rank + 1)) == float(world)
-        # sharded filter: rank r sums its contiguous nodes in ascending order
+        # no GPU here: the multi-rank context must fail loudly, never fall back
+        try:
+            D.make_context(rank, world, 0)
+            raise AssertionError("make_context succeeded without a GPU")
+        except P.FeastCudaError:
+            pass
+        # the product's rule (host C++) is bitwise rank-invariant
         n, p, nc = 40, 3, 8
+        rule = P.build_contour_rule(P.SearchInterval(-0.5, 0.5), nc)
+        zr, zi, wr, wi = (np.ascontiguousarray(v) for v in rule.parts())
+        mine = torch.from_numpy(np.concatenate([zr, zi, wr, wi]))
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        assert all(torch.equal(allr[0], t) for t in allr)
+        # sharded filter: rank r sums its contiguous nodes in ascending order
         A = O.random_symmetric(n, 77) / np.sqrt(n)
         X = O.random_block(n, p, 78)
-        rule = O.build_contour_rule(O.SearchInterval(-0.5, 0.5), nc)
+        orule = O.contour_rule_from_nodes(O.SearchInterval(-0.5, 0.5), list(zr + 1j * zi),
+                                          list(wr + 1j * wi))
         kb, ke = D.node_shard(nc, rank, world)
-        part = O.ContourRule(rule.interval, rule.nodes[kb:ke], rule.weights[kb:ke])
+        part = O.ContourRule(orule.interval, orule.nodes[kb:ke], orule.weights[kb:ke])
         Y = O.apply_filter(A, part, X) if ke > kb else np.zeros((n, p))
         t = torch.from_numpy(np.ascontiguousarray(Y))
         dist.all_reduce(t)
         if rank == 0:
-            full = O.apply_filter(A, rule, X)
+            full = O.apply_filter(A, orule, X)
             out.put(("ok", float(np.linalg.norm(t.numpy() - full) / np.linalg.norm(full))))
-    except Exception as e:  # report to the parent
+    except BaseException as e:  # report to the parent
         out.put(("err", repr(e)))
     finally:
         dist.destroy_process_group()
@@ -67,11 +91,12 @@ def test_node_shards_partition_the_rule():
         D.node_shard(8, 2, 2)
 
 
-def test_two_rank_sharded_filter_sum_gloo():
+@pytest.mark.parametrize("world", [2, 4])
+def test_multirank_host_path_and_sharded_filter_sum_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
