@@ -39,6 +39,38 @@ def lib():
     return _lib
 
 
+# The reference's own sources compiled against oracle/eigen_shim (`make -C
+# oracle ref`, needs /root/reference): same orc_* entry points, so every
+# function below can run on it. Present only where it was built.
+_REF_PATH = os.path.join(_HERE, "_ref", "libfeastlab_ref.so")
+_ref_lib = None
+
+
+def reference_available() -> bool:
+    return os.path.exists(_REF_PATH)
+
+
+class reference_backend:
+    """with oracle.reference_backend(): ...  -- route this module's calls to
+    oracle/_ref/libfeastlab_ref.so (the reference's unmodified sources)."""
+
+    def __enter__(self):
+        global _lib, _ref_lib
+        if _ref_lib is None:
+            _ref_lib = C.CDLL(_REF_PATH)
+            _declare(_ref_lib, optional=("orc_gaussian_fill", "orc_uniform_fill",
+                                         "orc_seeded_orthogonal", "orc_node_factor"))
+        lib()
+        self._saved = _lib
+        _lib = _ref_lib
+        return self
+
+    def __exit__(self, *exc):
+        global _lib
+        _lib = self._saved
+        return False
+
+
 # --------------------------------------------------------------- errors
 class InvalidArgument(ValueError):
     """std::invalid_argument"""
@@ -99,7 +131,7 @@ _LL = C.c_longlong
 _ULL = C.c_ulonglong
 
 
-def _declare(L):
+def _declare(L, optional=()):
     sig = {
         "orc_set_threads": (None, [_I]),
         "orc_get_threads": (_I, []),
@@ -125,6 +157,8 @@ def _declare(L):
                            _P]),
     }
     for name, (res, args) in sig.items():
+        if name in optional and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

@@ -5,7 +5,13 @@ minutes-to-hours of CPU work. Run in the build container.
 
 Usage:
   python tools/gen_golden.py <cfg> <threads> <driver>   -> tests/golden/parts/oracle_cfg<k>_<driver>.json
+  python tools/gen_golden.py <cfg> <threads> <driver> ref -> tests/golden/parts/ref_cfg<k>_<driver>.json
   python tools/gen_golden.py merge <cfg>                -> tests/golden/oracle_cfg<k>.json
+
+`ref` runs the same solve on oracle/_ref/libfeastlab_ref.so: the reference's
+own sources compiled unmodified against oracle/eigen_shim (`make -C oracle
+ref`). Its results are merged under "reference_build" and
+tests/test_ref_pin.py requires the restatement's goldens to agree with them.
 
 The goldens are generated with ONE OpenBLAS thread: the reference is built
 single-threaded (proj/CMakeLists.txt:6-13, no OpenMP), and the Gram-floor rank
@@ -60,14 +66,17 @@ def build_problem(idx, O, CF):
     return A, c
 
 
-def run(idx, threads, d):
+def run(idx, threads, d, ref=False):
+    import contextlib
     import oracle as O
     from paper_1605_08771_b200 import configs as CF
     O.set_threads(threads)
     A, c = build_problem(idx, O, CF)
     t = time.time()
-    s = getattr(O, d)(A, O.SearchInterval(c["lo"], c["hi"]),
-                      O.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"], s=c["s"]))
+    with (O.reference_backend() if ref else contextlib.nullcontext()):
+        s = getattr(O, d)(A, O.SearchInterval(c["lo"], c["hi"]),
+                          O.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"],
+                                         max_iter=c["max_iter"], s=c["s"]))
     e = {"seconds": round(time.time() - t, 2), "oracle_threads": O.get_threads(),
          "iterations": s.iterations, "converged": s.converged,
          "m": len(s.eigenvalues), "eigenvalues": [float(x) for x in s.eigenvalues],
@@ -75,10 +84,12 @@ def run(idx, threads, d):
          "rhs_solved": s.accounting.rhs_solved, "factorizations": s.accounting.factorizations,
          "trace": [[t.iter, t.subspace_dim, t.rhs_cumulative, t.max_residual, t.m_found] for t in s.trace],
          "r_over_tol": [t.max_residual / c["tol"] for t in s.trace]}
-    if d == "feast_solve" and s.first_filtered is not None:
+    if d == "feast_solve" and s.first_filtered is not None and not ref:
         e["first_filtered"] = first_sketch(s.first_filtered)
+    if ref:
+        e["library"] = "oracle/_ref/libfeastlab_ref.so (reference sources + oracle/eigen_shim)"
     os.makedirs(os.path.join(GOLD, "parts"), exist_ok=True)
-    with open(os.path.join(GOLD, "parts", f"oracle_cfg{idx}_{d}.json"), "w") as f:
+    with open(os.path.join(GOLD, "parts", f"{'ref' if ref else 'oracle'}_cfg{idx}_{d}.json"), "w") as f:
         json.dump({"cfg": idx, "config": c, "driver": d, "result": e}, f)
     print(idx, d, e["iterations"], e["converged"], e["m"], e["recovery_events"], e["seconds"], flush=True)
 
@@ -96,6 +107,12 @@ def merge(idx):
             ff.pop("full_shape")
         out["drivers"][part["driver"]] = res
     out["oracle_threads"] = max(e["oracle_threads"] for e in out["drivers"].values())
+    out["reference_build"] = {}
+    for p in sorted(glob.glob(os.path.join(GOLD, "parts", f"ref_cfg{idx}_*.json"))):
+        part = json.load(open(p))
+        res = part["result"]
+        res.pop("residual_norms", None)  # keep the fixture small: outcomes, trace, eigenvalues
+        out["reference_build"][part["driver"]] = res
     with open(os.path.join(GOLD, f"oracle_cfg{idx}.json"), "w") as f:
         json.dump(out, f)
     print("wrote", idx, sorted(out["drivers"]))
@@ -105,4 +122,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "merge":
         merge(int(sys.argv[2]))
     else:
-        run(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3])
+        run(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], ref=(len(sys.argv) > 4 and sys.argv[4] == "ref"))
