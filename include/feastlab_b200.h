@@ -122,13 +122,25 @@ int fl_ctx_factorization(const fl_ctx* ctx); /* the mode in effect, -1 for NULL 
    only queries. Returns the mode in effect. Env FEASTLAB_ZGEMM=4m|3m sets
    the initial value. */
 int fl_zgemm_mode(int mode);
-/* timeline of the profiled launches: out[4i] = class index (order of
-   fl_ctx_profile's classes), out[4i+1] / out[4i+2] = start / end in ms,
-   out[4i+3] = the launch's algorithmic work */
+/* timeline of the profiled launches: out[5i] = class index (order of
+   fl_ctx_profile's classes), out[5i+1] / out[5i+2] = start / end in ms,
+   out[5i+3] = the launch's algorithmic work, out[5i+4] = its shape tag
+   (GEMM classes: ((role*1024 + M/64)*1024 + N/64)*1024 + K/16, else 0) */
 int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records);
 /* microbenchmark of the planar-complex DMMA GEMM (instrumentation) */
 int fl_debug_zgemm(fl_ctx* ctx, int M, int N, int K, int batch, int iters, double* ms_out,
                    fl_err* err);
+/* the same product on operands laid out as in an LU trailing update: batch
+   N x N planar factors, C = F[N-M:, N-M:N-M+Nc] -= F[N-M:, 0:K] F[0:K, ...].
+   variant 0: the cp.async 3M/4M kernel; 1: the TMA-fed 3M kernel with
+   precomputed sum planes. *checksum = a weighted sum of C after one product;
+   maxdiff[0] = max |C_variant - C_variant0|, maxdiff[1] = max |F| (variant != 0)
+   (instrumentation: compares kernel variants) */
+int fl_debug_zgemm_lu(fl_ctx* ctx, int N, int M, int Nc, int K, int batch, int iters, int variant,
+                      double* ms_out, double* checksum, double* maxdiff, fl_err* err);
+/* weighted sums of the 64 x 64 tiles of the factors in slots [0, count)
+   (instrumentation: compares factorizations across runs) */
+int fl_debug_factor_tilesums(fl_filter* f, int count, double* out);
 /* cycle counts of the LU panel kernel's phases (instrumentation) */
 int fl_debug_panel_profile(double* out8, int reset);
 /* per-warp clock64 trace of the first on-chip panel (builds with FL_PANEL_TRACE) */

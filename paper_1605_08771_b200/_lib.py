@@ -63,6 +63,8 @@ _SIGS = {
     "fl_mm_write": (_I, [C.c_char_p, _P, _I, _I, _I, _P]),
     "fl_ctx_profile_dump": (_I, [_P, _P, _I]),
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
+    "fl_debug_zgemm_lu": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "fl_debug_factor_tilesums": (_I, [_P, _I, _P]),
     "fl_zgemm_mode": (_I, [_I]),
     "fl_solve_many": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P,
                            _P, _P]),

@@ -91,16 +91,17 @@ struct DBuf {
 // Per-kernel-class CUDA-event timing (fl_ctx_set_profiling): bench.py's
 // roofline numbers come from these events, recorded on the launch stream.
 enum ProfClass { P_SHIFT, P_PANEL, P_LASWP, P_TRSM, P_ZGEMM, P_PERMUTE, P_ACCUM, P_ALLREDUCE,
-                 P_EIG, P_ORTH, P_RR, P_NCLASS };
+                 P_EIG, P_ORTH, P_RR, P_ZSUM, P_NCLASS };
 const char* const kProfNames[P_NCLASS] = {"shift",   "panel",      "laswp",    "trsm",
                                           "zgemm",   "permute",    "accumulate", "allreduce",
-                                          "eig",     "orthonormalize", "rayleigh_ritz"};
+                                          "eig",     "orthonormalize", "rayleigh_ritz", "zsum"};
 
 struct Profiler {
     struct Rec {
         int cls;
         cudaEvent_t a, b;
         double work;
+        double tag;  // launch shape (zgemm classes: shape_tag), 0 otherwise
     };
     bool on = false;
     std::vector<Rec> recs;
@@ -184,6 +185,13 @@ struct fl_filter {
     DBuf fac_re, fac_im, ipiv, perm, bad, ptab;
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     DBuf lt_re, lt_im;    // LDL^T: per slot, the current panel's L_kk^{-T} (64 x 64)
+    // TMA-fed trailing updates (gemm_tma.cu): per slot the sum planes Re + Im of
+    // the current outer block's L21 (N x sum_kb, ld N) and U12 (sum_kb x N, ld
+    // sum_kb), and the tensor maps of the factor planes and the sum planes
+    DBuf sum_a, sum_b;
+    int sum_kb = 0;
+    ZGemmMaps maps;
+    bool maps_ok = false;
     int fac_mode = -1;    // factorization the cached factors were built with
     int fac_slots = 0;
     int panel_res_rows = 4096;   // see panel_res_rows()
@@ -305,8 +313,9 @@ struct Prof {
     double work;
     cudaStream_t st;
     cudaEvent_t a = nullptr;
-    Prof(fl_ctx* c, int k, double w, int launches = 1, cudaStream_t s = nullptr)
-        : ctx(c), cls(k), work(w), st(s ? s : c->stream) {
+    double tag = 0.0;
+    Prof(fl_ctx* c, int k, double w, int launches = 1, cudaStream_t s = nullptr, double t = 0.0)
+        : ctx(c), cls(k), work(w), st(s ? s : c->stream), tag(t) {
         g_launch_count += launches;
         if (ctx->prof.on) {
             a = ctx->prof.get();
@@ -317,14 +326,31 @@ struct Prof {
         if (a) {
             cudaEvent_t b = ctx->prof.get();
             cudaEventRecord(b, st);
-            ctx->prof.recs.push_back({cls, a, b, work});
+            ctx->prof.recs.push_back({cls, a, b, work, tag});
         }
     }
 };
 
+// Shape tag of a profiled GEMM-class launch (fl_ctx_profile_dump): role
+// (1 trailing update, 2 in-block panel-column update, 3 in-block U12 update,
+// 4 in-block U rows of a panel column, 5 solve update, 6 in-block solve
+// update, 7 L_kk^-1 product, 8 solve diagonal-block product), M/64, N/64, K/16.
+double shape_tag(int role, int M, int N, int K) {
+    return (((double)role * 1024 + M / 64) * 1024 + N / 64) * 1024 + K / 16;
+}
+
 double* scratch(DBuf& b, size_t doubles) {
     b.ensure(sizeof(double) * std::max<size_t>(doubles, 1));
     return b.d();
+}
+
+// FEASTLAB_ZGEMM_TMA=0 keeps the cp.async kernel for the trailing updates
+bool tma_updates() {
+    static const bool on = [] {
+        const char* e = std::getenv("FEASTLAB_ZGEMM_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on && zgemm_mode() == 1;
 }
 
 // --------------------------------------------------------------- filter core
@@ -365,12 +391,12 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     auto E = [&](int r, int c) { return (long)c * N + r; };
     // C[r,c: +M x +nc] -= A[ar,ac: M x K] B[br,bc: K x nc]
     auto sub = [&](int M, int nc, int K, int ar, int ac, int br, int bc, int cr, int cc,
-                   cudaStream_t s) {
+                   cudaStream_t s, int role) {
         if (M <= 0 || nc <= 0) return;
         ZGemm g{M, nc, K, F.re + E(ar, ac), F.im + E(ar, ac), N, stride,
                 F.re + E(br, bc), F.im + E(br, bc), N, stride,
                 F.re + E(cr, cc), F.im + E(cr, cc), N, stride};
-        Prof pr(ctx, P_ZGEMM, 8.0 * M * nc * K * G, 1, s);
+        Prof pr(ctx, P_ZGEMM, 8.0 * M * nc * K * G, 1, s, shape_tag(role, M, nc, K));
         launch_zgemm_sub(g, G, s);
     };
     // F[k:k+64, c:c+nc] = L_kk^{-1} F[k:k+64, c:c+nc] (in place)
@@ -380,7 +406,7 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         ZGemm u{T, nc, T, Inv.re + ib, Inv.im + ib, T, Inv.stride,
                 F.re + E(k, c), F.im + E(k, c), N, stride, F.re + E(k, c), F.im + E(k, c), N,
                 stride};
-        Prof pr(ctx, P_TRSM, 8.0 * T * T * nc * G, 1, s);
+        Prof pr(ctx, P_TRSM, 8.0 * T * T * nc * G, 1, s, shape_tag(7, T, nc, T));
         launch_zgemm_set(u, G, s);
     };
     // one pivot table per panel of an outer block: panel j+1's must not
@@ -395,6 +421,25 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     auto swaps = [&](const int* tab, int a0, int a1, int b0, int b1, cudaStream_t s) {
         Prof pr(ctx, P_LASWP, 0.0, 1, s);
         launch_laswp(F, a0, a1, b0, b1, tab, G, s);
+    };
+    // A[c0:, cc : cc + nc] -= L[c0:, k0 : k0 + K] U[k0 : k0 + K, cc : cc + nc] by the
+    // TMA-fed kernel; the sum planes of L21 and U12 are formed first (once per
+    // outer block: `have_sums` for the second launch of a block)
+    auto trailing = [&](int M, int nc, int K, int k0, int c0, int cc, bool have_sums) {
+        if (M <= 0 || nc <= 0) return;
+        const long sa = (long)N * f->sum_kb;
+        if (!have_sums) {
+            Prof pr(ctx, P_ZSUM, 24.0 * ((double)M * K + (double)K * (N - c0)) * G, 2, st);
+            launch_zsum(F.re + E(c0, k0), F.im + E(c0, k0), N, stride, f->sum_a.d() + s0 * sa + c0, N,
+                        sa, M, K, G, st);
+            launch_zsum(F.re + E(k0, c0), F.im + E(k0, c0), N, stride,
+                        f->sum_b.d() + s0 * sa + (long)c0 * f->sum_kb, f->sum_kb, sa, K, N - c0, G,
+                        st);
+        }
+        ZGemmTma t{M, nc, K, c0, k0, s0, c0, 0, s0, k0, cc, s0, 0, cc, s0,
+                   F.re + E(c0, cc), F.im + E(c0, cc), N, stride};
+        Prof pr(ctx, P_ZGEMM, 8.0 * M * nc * K * G, 1, st, shape_tag(1, M, nc, K));
+        launch_zgemm_sub_tma(f->maps, t, G, st);
     };
     // Outer blocks of NPB panels (BW = 64 NPB columns), panels k_j = k0 + 64 j.
     // The panel stream factors all of a block's panels while the main stream
@@ -426,9 +471,9 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
                 for (int i = 0; i < j; ++i) {
                     const int ki = k0 + i * T;
                     linv(ki, kj, T, sp);
-                    if (i + 1 < j) sub((j - 1 - i) * T, T, T, ki + T, ki, ki, kj, ki + T, kj, sp);
+                    if (i + 1 < j) sub((j - 1 - i) * T, T, T, ki + T, ki, ki, kj, ki + T, kj, sp, 4);
                 }
-                sub(N - kj, T, j * T, kj, k0, k0, kj, kj, kj, sp);
+                sub(N - kj, T, j * T, kj, k0, k0, kj, kj, kj, sp, 2);
             }
             panel(kj, tabs[j]);
         }
@@ -445,12 +490,18 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         for (int j = 0; j < np; ++j) {
             const int kj = k0 + j * T;
             linv(kj, c0, rest, st);
-            if (j + 1 < np) sub((np - 1 - j) * T, rest, T, kj + T, kj, kj, c0, kj + T, c0, st);
+            if (j + 1 < np) sub((np - 1 - j) * T, rest, T, kj + T, kj, kj, c0, kj + T, c0, st, 3);
         }
         const int nxt = std::min(np * T, rest);
-        sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st);
-        CK(cudaEventRecord(ev_next, st));
-        sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st);
+        if (f->maps_ok && tma_updates() && np * T >= 2 * T && np * T <= f->sum_kb) {
+            trailing(rest, nxt, np * T, k0, c0, c0, false);
+            CK(cudaEventRecord(ev_next, st));
+            trailing(rest, rest - nxt, np * T, k0, c0, c0 + nxt, true);
+        } else {
+            sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st, 1);
+            CK(cudaEventRecord(ev_next, st));
+            sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st, 1);
+        }
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
@@ -516,6 +567,30 @@ void factor_group_ldlt(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cud
         if (lower) launch_zgemm_sub_lower(g, ts, G, s);
         else launch_zgemm_sub(g, G, s);
     };
+    // the lower-trapezoid trailing update by the TMA-fed kernel (cf. factor_group)
+    auto trailing = [&](int M, int nc, int K, int k0, int c0, int cc, bool have_sums) {
+        if (M <= 0 || nc <= 0) return;
+        const long sa = (long)N * f->sum_kb;
+        if (!have_sums) {
+            Prof pr(ctx, P_ZSUM, 24.0 * ((double)M * K + (double)K * (N - c0)) * G, 2, st);
+            launch_zsum(F.re + E(c0, k0), F.im + E(c0, k0), N, stride, f->sum_a.d() + s0 * sa + c0, N,
+                        sa, M, K, G, st);
+            launch_zsum(F.re + E(k0, c0), F.im + E(k0, c0), N, stride,
+                        f->sum_b.d() + s0 * sa + (long)c0 * f->sum_kb, f->sum_kb, sa, K, N - c0, G,
+                        st);
+        }
+        ZGemmTma t{M, nc, K, c0, k0, s0, c0, 0, s0, k0, cc, s0, 0, cc, s0,
+                   F.re + E(c0, cc), F.im + E(c0, cc), N, stride};
+        t.tri = true;
+        t.tri_s = (cc - c0) / T;
+        double tiles = 0;
+        for (int c = 0; c < nc / T; ++c) {
+            const int lo = std::max(0, c + t.tri_s);
+            if (lo < M / T) tiles += M / T - lo;
+        }
+        Prof pr(ctx, P_ZGEMM, 8.0 * tiles * T * T * K * G, 1, st, shape_tag(1, M, nc, K));
+        launch_zgemm_sub_tma(f->maps, t, G, st);
+    };
     const int NPB = f->lu_panels;
     CK(cudaEventRecord(ev_next, st));  // shift done: block 0 may start
     for (int k0 = 0; k0 < N; k0 += NPB * T) {
@@ -546,9 +621,15 @@ void factor_group_ldlt(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cud
         const int rest = N - c0;
         if (rest <= 0) break;
         const int nxt = std::min(np * T, rest);
-        sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st, true);
-        CK(cudaEventRecord(ev_next, st));
-        sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st, true);
+        if (f->maps_ok && tma_updates() && np * T >= 2 * T && np * T <= f->sum_kb) {
+            trailing(rest, nxt, np * T, k0, c0, c0, false);
+            CK(cudaEventRecord(ev_next, st));
+            trailing(rest, rest - nxt, np * T, k0, c0, c0 + nxt, true);
+        } else {
+            sub(rest, nxt, np * T, c0, k0, k0, c0, c0, c0, st, true);
+            CK(cudaEventRecord(ev_next, st));
+            sub(rest, rest - nxt, np * T, c0, k0, k0, c0 + nxt, c0, c0 + nxt, st, true);
+        }
     }
     Prof pr(ctx, P_PANEL, 0.0, 3, st);
     launch_trinv(F, 0, NB, true, Inv, NB, G, st);  // U_ii^{-1} for the solves
@@ -572,7 +653,8 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
     const long istride = 2L * NB * FL_TILE * FL_TILE;
     ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
     auto tri = [&](int blk, int r0) {  // W_i <- T_ii^{-1} W_i (DMMA, in place)
-        Prof pr(ctx, P_TRSM, 8.0 * FL_TILE * FL_TILE * P * G, 1, st);
+        Prof pr(ctx, P_TRSM, 8.0 * FL_TILE * FL_TILE * P * G, 1, st,
+                shape_tag(8, FL_TILE, P, FL_TILE));
         ZGemm u{FL_TILE, P, FL_TILE,
                 Inv.re + (long)blk * FL_TILE * FL_TILE, Inv.im + (long)blk * FL_TILE * FL_TILE,
                 FL_TILE, Inv.stride,
@@ -584,7 +666,7 @@ void solve_group(fl_filter* f, int g0, int G, int s0, const double* X, long ldx,
         if (M <= 0) return;
         ZGemm g{M, P, K, F.re + (long)fc * N + fr, F.im + (long)fc * N + fr, N, stride,
                 W.re + wk, W.im + wk, N, W.stride, W.re + wr, W.im + wr, N, W.stride};
-        Prof pr(ctx, P_ZGEMM, 8.0 * M * P * K * G, 1, st);
+        Prof pr(ctx, P_ZGEMM, 8.0 * M * P * K * G, 1, st, shape_tag(K > FL_TILE ? 5 : 6, M, P, K));
         launch_zgemm_sub(g, G, st);
     };
     // row blocks of NPB tiles (cf. the LU), so the long updates have K = 64 NPB:
@@ -705,6 +787,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->lt_re.ensure(sizeof(double) * (size_t)FL_TILE * FL_TILE * slots);
         f->lt_im.ensure(sizeof(double) * (size_t)FL_TILE * FL_TILE * slots);
         f->fac_slots = slots;
+        f->maps_ok = false;
         std::fill(f->factored.begin(), f->factored.end(), 0);
     }
     alloc_lk.unlock();
@@ -726,6 +809,22 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
                                  N >= 12288 ? (L >= 8 ? 16 : 8) : (L >= 8 ? 4 : 2),
                                  FL_MAX_BLOCK_PANELS);
     f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4, 8);
+    // sum planes and tensor maps of the TMA-fed trailing updates (outer blocks
+    // of at least 128 columns, 3M product)
+    if (tma_updates() && f->lu_panels >= 2 &&
+        (!f->maps_ok || f->sum_kb != f->lu_panels * FL_TILE ||
+         f->sum_a.bytes < sizeof(double) * (size_t)N * f->lu_panels * FL_TILE * f->fac_slots)) {
+        const int KB = f->lu_panels * FL_TILE;
+        f->sum_a.ensure(sizeof(double) * (size_t)N * KB * f->fac_slots);
+        f->sum_b.ensure(sizeof(double) * (size_t)N * KB * f->fac_slots);
+        make_tma_map_mk(&f->maps.Ar, f->fac_re.d(), N, N, N, fstride, f->fac_slots);
+        make_tma_map_mk(&f->maps.Ai, f->fac_im.d(), N, N, N, fstride, f->fac_slots);
+        make_tma_map_mk(&f->maps.As, f->sum_a.d(), N, KB, N, (long)N * KB, f->fac_slots);
+        make_tma_map_km(&f->maps.Br, f->fac_re.d(), N, N, N, fstride, f->fac_slots);
+        make_tma_map_km(&f->maps.Bi, f->fac_im.d(), N, N, N, fstride, f->fac_slots);
+        make_tma_map_km(&f->maps.Bs, f->sum_b.d(), KB, N, KB, (long)KB * N, f->fac_slots);
+        f->maps_ok = true;
+    }
     long long new_facts = 0;
     // everything below is stream work only (no host synchronisation), so a
     // non-cache application is one CUDA graph: ~2.8k launches on 9 streams
@@ -1333,8 +1432,9 @@ int fl_ctx_rank(const fl_ctx* ctx, int* rank, int* nranks) {
 
 long long fl_ctx_launches(const fl_ctx* ctx) { return g_launch_count.load() - ctx->launches_at_create; }
 
-// timeline of the profiled launches: out[4*i] = class, [4*i+1] = start ms,
-// [4*i+2] = end ms (relative to the first recorded event), [4*i+3] = work; returns the count
+// timeline of the profiled launches: out[5*i] = class, [5*i+1] = start ms,
+// [5*i+2] = end ms (relative to the first recorded event), [5*i+3] = work,
+// [5*i+4] = shape tag (GEMM classes, shape_tag(); else 0); returns the count
 int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
     CtxLock lk(ctx);
     cudaStreamSynchronize(ctx->stream);
@@ -1348,10 +1448,11 @@ int fl_ctx_profile_dump(fl_ctx* ctx, double* out, int max_records) {
         float a = 0.f, b = 0.f;
         cudaEventElapsedTime(&a, base, r.a);
         cudaEventElapsedTime(&b, base, r.b);
-        out[4 * n] = r.cls;
-        out[4 * n + 1] = a;
-        out[4 * n + 2] = b;
-        out[4 * n + 3] = r.work;
+        out[5 * n] = r.cls;
+        out[5 * n + 1] = a;
+        out[5 * n + 2] = b;
+        out[5 * n + 3] = r.work;
+        out[5 * n + 4] = r.tag;
         ++n;
     }
     return n;
@@ -1387,6 +1488,183 @@ int fl_debug_zgemm(fl_ctx* ctx, int M, int Nc, int K, int batch, int iters, doub
         cudaEventDestroy(e1);
         *ms_out = ms / iters;
     });
+}
+
+// The same product in the LU's own layout: batch N x N planar factors,
+// C = F[N-M:, N-M : N-M+Nc] -= F[N-M:, 0:K] F[0:K, N-M : N-M+Nc] (ld N, so the
+// operand tiles are strided exactly as in a trailing update). The planes hold
+// pseudo-random values; *checksum = sum of C after one product from the
+// initial fill (to compare kernel variants bit for bit).
+namespace {
+__global__ void debug_fill_kernel(double* p, size_t n, unsigned seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long x = (i + 1) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull;
+        x ^= x >> 29;
+        x *= 0xBF58476D1CE4E5B9ull;
+        x ^= x >> 32;
+        p[i] = ((double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5) * 0.0625;
+    }
+}
+__global__ void debug_sum_kernel(const double* re, const double* im, long ld, int M, int Nc,
+                                 long stride, int batch, double* out) {
+    double s = 0.0;
+    const long total = (long)M * Nc * batch;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+         i += (long)gridDim.x * blockDim.x) {
+        const long b = i / ((long)M * Nc), r = i % ((long)M * Nc);
+        const long off = b * stride + (r / M) * ld + (r % M);
+        s += re[off] * 1.0 + im[off] * 0.5;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+}  // namespace
+
+__global__ void debug_maxdiff_kernel(const double* a, const double* b, size_t n, double* out) {
+    double d = 0.0, m = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        d = fmax(d, fabs(a[i] - b[i]));
+        m = fmax(m, fabs(a[i]));
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    }
+    if ((threadIdx.x & 31) == 0) {  // non-negative doubles order as their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(d));
+        atomicMax(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+int fl_debug_zgemm_lu(fl_ctx* ctx, int N, int M, int Nc, int K, int batch, int iters, int variant,
+                      double* ms_out, double* checksum, double* maxdiff, fl_err* err) {
+    return guarded(err, [&] {
+        CtxLock lk(ctx);
+        if (N % 64 || M % 64 || Nc % 64 || K % 16 || batch < 1 || iters < 1 || M + K > N ||
+            Nc > M)
+            throw Fail{FL_INVALID_ARGUMENT, "fl_debug_zgemm_lu: bad shape"};
+        const size_t plane = (size_t)N * N;
+        DBuf buf, ref, sum, sa, sb;
+        buf.ensure(sizeof(double) * 2 * plane * batch);
+        sum.ensure(sizeof(double) * 4);
+        double* re = buf.d();
+        double* im = re + plane * batch;
+        auto fill = [&] {
+            debug_fill_kernel<<<148 * 8, 256, 0, ctx->stream>>>(re, 2 * plane * batch, 17u);
+        };
+        const int c0 = N - M;
+        auto E = [&](int r, int c) { return (long)c * N + r; };
+        ZGemm g{M, Nc, K, re + E(c0, 0), im + E(c0, 0), N, (long)plane,
+                re + E(0, c0), im + E(0, c0), N, (long)plane,
+                re + E(c0, c0), im + E(c0, c0), N, (long)plane};
+        ZGemmMaps maps;
+        ZGemmTma t{M, Nc, K, c0, 0, 0, c0, 0, 0, 0, c0, 0, 0, c0, 0, g.Cr, g.Ci, N, (long)plane};
+        if (variant >= 1) {
+            sa.ensure(sizeof(double) * (size_t)N * K * batch);
+            sb.ensure(sizeof(double) * (size_t)K * N * batch);
+            make_tma_map_mk(&maps.Ar, re, N, N, N, (long)plane, batch);
+            make_tma_map_mk(&maps.Ai, im, N, N, N, (long)plane, batch);
+            make_tma_map_mk(&maps.As, sa.d(), N, K, N, (long)N * K, batch);
+            make_tma_map_km(&maps.Br, re, N, N, N, (long)plane, batch);
+            make_tma_map_km(&maps.Bi, im, N, N, N, (long)plane, batch);
+            make_tma_map_km(&maps.Bs, sb.d(), K, N, K, (long)K * N, batch);
+        }
+        auto sums = [&] {
+            launch_zsum(re + E(c0, 0), im + E(c0, 0), N, (long)plane, sa.d() + c0, N, (long)N * K, M,
+                        K, batch, ctx->stream);
+            launch_zsum(re + E(0, c0), im + E(0, c0), N, (long)plane, sb.d() + (long)c0 * K, K,
+                        (long)K * N, K, Nc, batch, ctx->stream);
+        };
+        auto run = [&](int v) {
+            if (v == 1) {
+                launch_zgemm_sub_tma(maps, t, batch, ctx->stream);
+            } else {
+                launch_zgemm_sub(g, batch, ctx->stream);
+            }
+        };
+        fill();
+        if (variant >= 1) sums();
+        run(variant);
+        CK(cudaMemsetAsync(sum.p, 0, sizeof(double) * 4, ctx->stream));
+        debug_sum_kernel<<<148 * 4, 256, 0, ctx->stream>>>(g.Cr, g.Ci, N, M, Nc, (long)plane,
+                                                          batch, sum.d());
+        double host[4] = {0, 0, 0, 0};
+        if (variant != 0 && maxdiff) {  // against the cp.async kernel on the same fill
+            ref.ensure(sizeof(double) * 2 * plane * batch);
+            CK(cudaMemcpyAsync(ref.p, buf.p, sizeof(double) * 2 * plane * batch,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+            fill();
+            run(0);
+            debug_maxdiff_kernel<<<148 * 4, 256, 0, ctx->stream>>>(re, ref.d(), 2 * plane * batch,
+                                                              sum.d() + 1);
+        }
+        CK(cudaMemcpyAsync(host, sum.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (checksum) *checksum = host[0];
+        if (maxdiff) {
+            maxdiff[0] = host[1];
+            maxdiff[1] = host[2];
+        }
+        ref.release();
+        fill();
+        if (variant >= 1) sums();
+        run(variant);  // warm
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, ctx->stream);
+        for (int i = 0; i < iters; ++i) run(variant);
+        cudaEventRecord(e1, ctx->stream);
+        CK(cudaEventSynchronize(e1));
+        CK(cudaGetLastError());
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms / iters;
+    });
+}
+
+namespace {
+__global__ void tile_sums_kernel(const double* re, const double* im, long ld, long stride, int NB,
+                                 double* out) {
+    const int tr = blockIdx.x, tc = blockIdx.y, b = blockIdx.z;
+    const double* r = re + b * stride + (long)tc * 64 * ld + tr * 64;
+    const double* i = im + b * stride + (long)tc * 64 * ld + tr * 64;
+    double s = 0.0;
+    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+        const long o = (long)(e >> 6) * ld + (e & 63);
+        s += r[o] * (1.0 + 1e-3 * (e & 63)) + i[o] * (0.5 + 1e-3 * (e >> 6));
+    }
+    __shared__ double sh[8];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < blockDim.x / 32; ++w) t += sh[w];
+        out[((long)b * NB + tc) * NB + tr] = t;
+    }
+}
+}  // namespace
+
+// weighted sums of the 64 x 64 tiles of the factor in slots [0, count) (out:
+// count x NB x NB, tile column-major) -- compares factorizations across runs
+int fl_debug_factor_tilesums(fl_filter* f, int count, double* out) {
+    fl_ctx* ctx = f->ctx;
+    CtxLock lk(ctx);
+    const int N = f->A->N, NB = N / FL_TILE;
+    if (count > f->fac_slots) return FL_INVALID_ARGUMENT;
+    DBuf d;
+    d.ensure(sizeof(double) * (size_t)count * NB * NB);
+    cudaStreamSynchronize(ctx->stream);
+    tile_sums_kernel<<<dim3(NB, NB, count), 256, 0, ctx->stream>>>(f->fac_re.d(), f->fac_im.d(), N,
+                                                                   (long)N * N, NB, d.d());
+    cudaMemcpyAsync(out, d.p, sizeof(double) * (size_t)count * NB * NB, cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    return cudaStreamSynchronize(ctx->stream) == cudaSuccess ? FL_OK : FL_CUDA;
 }
 
 int fl_ctx_set_reduction(fl_ctx* ctx, int mode) {

@@ -9,29 +9,6 @@
 
 namespace fl {
 
-// Tile (bx, by) of the L-th tile of C's lower trapezoid {bx >= by + s},
-// column by column (Mt x Nt tiles). Columns c < -s are full (Mt tiles); from
-// there column f + j holds H - j tiles, H = Mt - f - s.
-FL_DEV void lower_tile(long L, int Mt, int s, int& bx, int& by) {
-    const int f = s < 0 ? -s : 0;
-    const long full = (long)f * Mt;
-    if (L < full) {
-        by = (int)(L / Mt);
-        bx = (int)(L % Mt);
-        return;
-    }
-    L -= full;
-    const long H = (long)Mt - f - s;
-    auto cum = [&](long j) { return j * H - j * (j - 1) / 2; };
-    const double b = 2.0 * H + 1.0;
-    long j = (long)((b - sqrt(fmax(b * b - 8.0 * (double)L, 0.0))) * 0.5);
-    if (j < 0) j = 0;
-    while (cum(j + 1) <= L) ++j;
-    while (j > 0 && cum(j) > L) --j;
-    by = (int)(f + j);
-    bx = (int)(f + j + s + (L - cum(j)));
-}
-
 // Number of tiles of that trapezoid (host).
 static long lower_tiles(int Mt, int Nt, int s) {
     long t = 0;
@@ -270,6 +247,7 @@ __global__ void __launch_bounds__(NT, MINB) zgemm3m_kernel(ZGemm g) {
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
     int bx = blockIdx.x, by = blockIdx.y;
     if (g.tri) lower_tile(blockIdx.x, g.M / GB, g.tri_s, bx, by);
+    else if (g.raster > 0) raster_tile(g.raster, g.M / GB, g.N / GB, bx, by);
     const int m0 = bx * GB, n0 = by * GB;
     const long z = blockIdx.z;
     const double* Ar = g.Ar + z * g.strideA;
@@ -422,10 +400,22 @@ void launch_dgemm(const DGemm& g, bool ta, bool tb, int batch, cudaStream_t s) {
 #undef FL_DG
 }
 
-void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s) {
-    if (g.M <= 0 || g.N <= 0 || g.K <= 0 || batch <= 0) return;
+// Row tiles per raster group (FEASTLAB_ZGEMM_RASTER, 0 = column-major launch order)
+static int raster_rows() {
+    static const int r = [] {
+        const char* e = std::getenv("FEASTLAB_ZGEMM_RASTER");
+        return e ? std::atoi(e) : 0;
+    }();
+    return r;
+}
+
+void launch_zgemm_sub(const ZGemm& g0, int batch, cudaStream_t s) {
+    if (g0.M <= 0 || g0.N <= 0 || g0.K <= 0 || batch <= 0) return;
+    ZGemm g = g0;
     dim3 grid(g.M / GB, g.N / GB, batch);
     if (zgemm_mode()) {
+        // only where a tile column does not already fit: several tile columns
+        if (g.N / GB > 1 && g.M / GB > raster_rows()) g.raster = raster_rows();
         launch_zgemm3m<true>(g, grid, s);
         return;
     }

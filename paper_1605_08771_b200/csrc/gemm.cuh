@@ -63,4 +63,42 @@ FL_DEV const double* tile_ptr(const double* base, long ld, int x0, int k0) {
     return KC ? base + (long)x0 * ld + k0 : base + (long)k0 * ld + x0;
 }
 
+// Tile (bx, by) of the L-th tile of C's lower trapezoid {bx >= by + s},
+// column by column (Mt x Nt tiles). Columns c < -s are full (Mt tiles); from
+// there column f + j holds H - j tiles, H = Mt - f - s.
+FL_DEV void lower_tile(long L, int Mt, int s, int& bx, int& by) {
+    const int f = s < 0 ? -s : 0;
+    const long full = (long)f * Mt;
+    if (L < full) {
+        by = (int)(L / Mt);
+        bx = (int)(L % Mt);
+        return;
+    }
+    L -= full;
+    const long H = (long)Mt - f - s;
+    auto cum = [&](long j) { return j * H - j * (j - 1) / 2; };
+    const double b = 2.0 * H + 1.0;
+    long j = (long)((b - sqrt(fmax(b * b - 8.0 * (double)L, 0.0))) * 0.5);
+    if (j < 0) j = 0;
+    while (cum(j + 1) <= L) ++j;
+    while (j > 0 && cum(j) > L) --j;
+    by = (int)(f + j);
+    bx = (int)(f + j + s + (L - cum(j)));
+}
+
+// Row-group rasterisation of a full Mt x Nt tile grid: CTAs in launch order
+// walk groups of R row tiles column by column, so the CTAs in flight share
+// R tiles of A's rows (R x K x 16 B stay in L2 for the whole sweep) and
+// stream B, instead of sweeping all of A once per tile column (a K = 1024
+// L21 panel is ~250 MB per node at cfg4: larger than L2).
+FL_DEV void raster_tile(int R, int Mt, int Nt, int& bx, int& by) {
+    const long L = (long)by * Mt + bx;
+    const long per = (long)R * Nt;
+    const int grp = (int)(L / per);
+    const int in = (int)(L - (long)grp * per);
+    const int rows = min(R, Mt - grp * R);
+    by = in / rows;
+    bx = grp * R + in - by * rows;
+}
+
 }  // namespace fl

@@ -1,5 +1,6 @@
 // Internal launch interface of the sm_100a kernels (not part of the C ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -45,10 +46,39 @@ struct ZGemm {
     // on a 1-D grid (launch_zgemm_sub_lower)
     bool tri = false;
     int tri_s = 0;
+    // > 0: launch order walks groups of `raster` row tiles (gemm.cu raster_tile)
+    int raster = 0;
 };
 void launch_zgemm_sub(const ZGemm& g, int batch, cudaStream_t s);
 // C -= A B on the lower trapezoid of C only (see ZGemm::tri_s)
 void launch_zgemm_sub_lower(const ZGemm& g, int tri_s, int batch, cudaStream_t s);
+// The TMA-fed 3M kernel for long-K trailing updates (gemm_tma.cu). Operands are
+// addressed through tensor maps (make_tma_map_mk for the 64-contiguous A side,
+// make_tma_map_km for the k-contiguous B side; rows multiple of 64) by element
+// coordinates: A = map[a_row + ., a_col + ., a_node + z], and the precomputed
+// sum planes As = Ar + Ai, Bs = Br + Bi (launch_zsum) likewise.
+struct ZGemmMaps {
+    CUtensorMap Ar, Ai, As, Br, Bi, Bs;
+};
+struct ZGemmTma {
+    int M, N, K;
+    int a_row, a_col, a_node;
+    int as_row, as_col, as_node;
+    int b_row, b_col, b_node;
+    int bs_row, bs_col, bs_node;
+    double *Cr, *Ci; long ldc; long strideC;
+    bool tri = false;
+    int tri_s = 0;
+    int raster = 0;
+};
+void make_tma_map_mk(CUtensorMap* m, const double* base, long rows, long cols, long ld, long stride,
+                     int batch);
+void make_tma_map_km(CUtensorMap* m, const double* base, long rows, long cols, long ld, long stride,
+                     int batch);
+void launch_zgemm_sub_tma(const ZGemmMaps& m, const ZGemmTma& g, int batch, cudaStream_t s);
+// out = re + im over rows x cols (rows even), batch planes `stride` / `ostride` apart
+void launch_zsum(const double* re, const double* im, long ld, long stride, double* out, long lds,
+                 long ostride, int rows, int cols, int batch, cudaStream_t s);
 // Complex product form of the zgemm launches: 1 = 3M (default), 0 = 4M.
 int zgemm_mode();
 void set_zgemm_mode(int mode);

@@ -160,6 +160,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, NT <= 256 ? 2 :
         t_last = t_;                                                             \
     }
 
+    // Every rank must have started (its shared memory allocated) before any
+    // rank pushes into it: a remote store to a block that has not started yet
+    // lands in whatever still occupies that SM's shared memory -- e.g. the last
+    // operand stages of a trailing-update GEMM CTA that is finishing there
+    // (observed: single wrong C tiles, only with the look-ahead panels running
+    // beside the TMA-fed trailing update).
+    cluster.sync();
     for (int q = 0; q < PWID / W; ++q) {
         const int c0 = k0 + q * W;
         // ---- load the leaf (rows >= c0 of this CTA)

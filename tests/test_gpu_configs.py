@@ -7,13 +7,8 @@
 * Converged results: eigenvalues within 1e-10 of the exact spectrum and the
   eigenvector subspace within max(1e-8, Davis-Kahan residual/gap bound) of
   the exact invariant subspace (see _check_exact).
-* XFEAST / RFEAST: their iteration counts hinge on Gram-floor rank and
-  selection decisions taken at the rounding level: the
-  oracle itself changes them when only OpenBLAS's thread count changes
-  (profiles/cfg1_oracle_thread_sensitivity.jsonl: XFEAST 11 vs 15 iterations).
-  So: first-iteration trace identical, and every converged result matches the
-  exact spectrum (count, eigenvalues 1e-10, subspace as above); when both sides
-  converge the eigenpairs must agree with each other too.
+* XFEAST / RFEAST: the same identities (iterations, converged, m,
+  recovery_events, full trace) against the one-thread oracle goldens.
 
 Oracle results for cfg0/cfg1 come from tests/golden/oracle_cfg*.json
 (tools/gen_golden.py); the exact eigenpairs are regenerated from the seeds.
@@ -32,7 +27,7 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
-@functools.lru_cache(maxsize=1)
+@functools.lru_cache(maxsize=2)
 def _fixture(index):
     """(A, exact eigenvalues, exact eigenvectors or None, resolved config),
     built on the host exactly as tools/gen_golden.py builds the oracle's
@@ -99,7 +94,7 @@ def _sketch(Y):
     return omega @ Y
 
 
-@pytest.mark.parametrize("index", [0, 2, 3, 4])
+@pytest.mark.parametrize("index", [0, 1, 2, 3, 4])
 def test_first_filtered_subspace_vs_golden_sketch(index, cfg0):
     """North-star gate ||Y1_gpu - Y1_ref||_F / ||Y1_ref||_F <= 1e-9 at the
     configurations whose Y1 is too large to commit: checked through the
@@ -124,61 +119,62 @@ def test_first_filtered_subspace_vs_golden_sketch(index, cfg0):
     assert abs(np.linalg.norm(Y) - ff["fro"]) <= 1e-9 * ff["fro"]
 
 
-@pytest.mark.parametrize("index", [0, 1, 2, 3, 4])
+def _trace(sol):
+    return [[t.iter, t.subspace_dim, t.rhs_cumulative, t.m_found] for t in sol.trace]
+
+
 @pytest.mark.parametrize("driver", ["feast_solve", "xfeast_solve", "rfeast_solve"])
+@pytest.mark.parametrize("index", [0, 1, 2, 3, 4])
 def test_drivers_vs_golden_oracle(index, driver, cfg0):
+    """North-star gate: identical iteration counts, converged counts, traces
+    (iter, subspace_dim, rhs_cumulative, m_found) and recovery events for every
+    driver on every configuration, against the one-thread oracle goldens (the
+    reference is built single-threaded, proj/CMakeLists.txt:6-13; the goldens of
+    cfg0 / cfg1 / cfg2-XFEAST are also reproduced by the reference's own
+    sources, tests/test_ref_pin.py). cfg4 holds FEAST only (hours per driver on
+    the CPU)."""
     import paper_1605_08771_b200 as P
-    drivers = _golden(index)["drivers"]
+    gold_all = _golden(index)
+    drivers = gold_all["drivers"]
     if driver not in drivers:
-        pytest.skip(f"cfg{index}: the golden holds {sorted(drivers)} (oracle minutes per driver)")
+        assert index == 4, f"cfg{index}: golden for {driver} missing"
+        pytest.skip("cfg4: the golden holds FEAST only (a CPU oracle run takes ~1 h per filter application)")
     gold = drivers[driver]
     A, vals, Q, c = cfg0 if index == 0 else _fixture(index)
     cfg = P.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"], s=c["s"])
     sol = getattr(P, driver)(A, P.SearchInterval(c["lo"], c["hi"]), cfg)
-    tr = [[t.iter, t.subspace_dim, t.rhs_cumulative, t.m_found] for t in sol.trace]
+    tr = _trace(sol)
     gtr = [[t[0], t[1], t[2], t[4]] for t in gold["trace"]]
-    print(f"cfg{index} {driver}: gpu {sol.iterations} it conv={sol.converged} m={len(sol.eigenvalues)}"
-          f" | oracle {gold['iterations']} it conv={gold['converged']} m={gold['m']}")
-    assert tr[0] == gtr[0]  # first iteration: same subspace size, accounting, inside count
-    if driver == "feast_solve" and gold["converged"]:
-        assert sol.iterations == gold["iterations"]
-        assert sol.converged == gold["converged"]
-        assert len(sol.eigenvalues) == gold["m"]
-        assert tr == gtr
+    print(f"cfg{index} {driver}: gpu {sol.iterations} it conv={sol.converged} m={len(sol.eigenvalues)} "
+          f"rec={sol.recovery_events} | oracle {gold['iterations']} it conv={gold['converged']} m={gold['m']} "
+          f"rec={gold['recovery_events']}")
+    for a, b, g in zip(tr, gtr, gold["trace"]):
+        if a != b:
+            print(f"  first differing record: gpu {a} oracle {b} (oracle max residual / tol {g[3] / c['tol']:.6e})")
+            break
+    assert sol.iterations == gold["iterations"]
+    assert sol.converged == gold["converged"]
+    assert len(sol.eigenvalues) == gold["m"]
+    assert sol.recovery_events == gold["recovery_events"]
+    assert tr == gtr
+    scale = max(np.abs(vals).max(), 1.0)
+    if gold["converged"]:
         ge = np.array(gold["eigenvalues"])
-        scale = np.maximum(np.abs(ge), max(np.abs(vals).max(), 1.0))
-        assert np.all(np.abs(sol.eigenvalues - ge) <= 1e-10 * scale)
-    elif driver == "feast_solve":
-        # The reference algorithm stagnates here (cfg1, cfg2: spurious Ritz
-        # pairs hold the max residual far above tol for all max_iter
-        # iterations, on the oracle too). Pinned: iteration and converged
-        # counts, the final count, subspace dims and accounting at every
-        # iteration; the inside count of a stagnating iteration may differ by
-        # a spurious pair sitting on the interval edge;
-        # converged pairs (residual <= 1e3 tol) agree to 1e-10.
-        assert sol.iterations == gold["iterations"]
-        assert sol.converged == gold["converged"]
-        assert len(sol.eigenvalues) == gold["m"]
-        assert [t[:3] for t in tr] == [t[:3] for t in gtr]
-        assert max(abs(a[3] - b[3]) for a, b in zip(tr, gtr)) <= 2
-        if index == 1:
-            assert tr == gtr  # cfg1's stagnating trace does agree exactly
+        assert np.all(np.abs(sol.eigenvalues - ge) <= 1e-10 * np.maximum(np.abs(ge), scale))
+        if Q is not None:
+            _check_exact(sol, vals, Q, c, A)
+    else:
+        # not converged on either side (the reference algorithm stagnates: spurious
+        # Ritz pairs hold the max residual above tol for all max_iter iterations):
+        # the pairs that did converge (residual <= 1e3 tol) agree to 1e-10
         ge, gr = np.array(gold["eigenvalues"]), np.array(gold["residual_norms"])
         good_g = np.sort(ge[gr <= 1e3 * c["tol"]])
         good = np.sort(np.asarray(sol.eigenvalues)[np.asarray(sol.residual_norms) <= 1e3 * c["tol"]])
-        k = min(len(good), len(good_g))
-        assert k >= 0.9 * max(len(good), len(good_g))
-        scale = max(np.abs(vals).max(), 1.0)
-        d = np.abs(good[:, None] - good_g[None, :]).min(axis=1)
-        print(f"  converged pairs {len(good)} vs {len(good_g)}, max |dlambda| {d.max():.2e}")
-        assert d.max() <= 1e-10 * scale
-    if sol.converged and Q is not None:
-        _check_exact(sol, vals, Q, c, A)
-    if sol.converged and gold["converged"]:
-        assert len(sol.eigenvalues) == gold["m"]
-        ge = np.array(gold["eigenvalues"])
-        assert np.abs(sol.eigenvalues - ge).max() <= 1e-10 * max(np.abs(vals).max(), 1.0)
-    if driver != "feast_solve":  # accounting formula (test_drivers.cpp:137-160)
+        if len(good) and len(good_g):
+            d = np.abs(good[:, None] - good_g[None, :]).min(axis=1)
+            print(f"  converged pairs {len(good)} vs {len(good_g)}, max |dlambda| {d.max():.2e}")
+            assert abs(len(good) - len(good_g)) <= 0.1 * max(len(good), len(good_g))
+            assert d.max() <= 1e-10 * scale
+    if driver == "xfeast_solve":  # accounting formula (proj/tests/test_drivers.cpp:137-160)
         for rec in sol.trace:
-            apps = rec.iter + (max(c["s"] - 2, 0) if driver == "xfeast_solve" else 0)
-            assert rec.rhs_cumulative == c["n_c"] * c["m0"] * apps
+            assert rec.rhs_cumulative == c["n_c"] * c["m0"] * (rec.iter + max(c["s"] - 2, 0))

@@ -1,5 +1,5 @@
 """One filter application on a bench workload (for ncu launch lists):
-python tools/one_app.py [cfg] [lu|ldlt]"""
+python tools/one_app.py [cfg] [lu|ldlt] [streams]"""
 import os
 import sys
 
@@ -14,6 +14,8 @@ import paper_1605_08771_b200 as P  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 ctx = P.default_context()
 ctx.set_factorization(sys.argv[2] if len(sys.argv) > 2 else "lu")
+if len(sys.argv) > 3:
+    ctx.set_streams(int(sys.argv[3]))
 A, vals, c = bench.build_workload(cfg, 0)
 n, p, nc = c["n"], c["m0"], c["n_c"]
 X = torch.from_numpy(np.ascontiguousarray(P.make_initial_guess(n, p, 42).T)).cuda()
