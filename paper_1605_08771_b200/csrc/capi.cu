@@ -817,6 +817,7 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         const int KB = f->lu_panels * FL_TILE;
         f->sum_a.ensure(sizeof(double) * (size_t)N * KB * f->fac_slots);
         f->sum_b.ensure(sizeof(double) * (size_t)N * KB * f->fac_slots);
+        f->sum_kb = KB;
         make_tma_map_mk(&f->maps.Ar, f->fac_re.d(), N, N, N, fstride, f->fac_slots);
         make_tma_map_mk(&f->maps.Ai, f->fac_im.d(), N, N, N, fstride, f->fac_slots);
         make_tma_map_mk(&f->maps.As, f->sum_a.d(), N, KB, N, (long)N * KB, f->fac_slots);

@@ -181,7 +181,12 @@ __global__ void __launch_bounds__(128, 2)
         const unsigned char* st = tiles + s * STAGE_B;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            if (c == 1 && tid == 0 && kt + LEAD < KT) produce(kt + LEAD);
+            // The producer role rotates over the four warps (tile t is issued by
+            // lane 0 of warp t & 3): both CTAs of an SM keep their warp w on
+            // sub-partition w, so a fixed producer warp would put all the TMA
+            // issue work of the SM on one sub-partition (FEASTLAB_TMA_ROTATE=0).
+            if (c == 1 && lane == 0 && warp == (g.rotate ? ((kt + LEAD) & 3) : 0) && kt + LEAD < KT)
+                produce(kt + LEAD);
             double ar[4], ai[4], as[4], br[4], bi[4], bs[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -366,6 +371,11 @@ void launch_zgemm_sub_tma(const ZGemmMaps& m, const ZGemmTma& g0, int batch, cud
     } else if (g.N / GB > 1 && g.M / GB > tma_raster_rows()) {
         g.raster = tma_raster_rows();
     }
+    static const int rotate = [] {
+        const char* e = std::getenv("FEASTLAB_TMA_ROTATE");
+        return e ? std::atoi(e) : 1;
+    }();
+    g.rotate = rotate;
     ensure_smem((const void*)zgemm3s_kernel<true>, TMA_SMEM);
     zgemm3s_kernel<true><<<grid, 128, TMA_SMEM, s>>>(m.Ar, m.Ai, m.As, m.Br, m.Bi, m.Bs, g);
 }

@@ -70,6 +70,7 @@ struct ZGemmTma {
     bool tri = false;
     int tri_s = 0;
     int raster = 0;
+    int rotate = 1;  // producer role rotates over the warps (gemm_tma.cu)
 };
 void make_tma_map_mk(CUtensorMap* m, const double* base, long rows, long cols, long ld, long stride,
                      int batch);

@@ -6,6 +6,7 @@ minutes-to-hours of CPU work. Run in the build container.
 Usage:
   python tools/gen_golden.py <cfg> <threads> <driver>   -> tests/golden/parts/oracle_cfg<k>_<driver>.json
   python tools/gen_golden.py <cfg> <threads> <driver> ref -> tests/golden/parts/ref_cfg<k>_<driver>.json
+  python tools/gen_golden.py <cfg> <threads> <driver> sens -> tests/golden/parts/sens_cfg<k>_<driver>.json
   python tools/gen_golden.py merge <cfg>                -> tests/golden/oracle_cfg<k>.json
 
 `ref` runs the same solve on oracle/_ref/libfeastlab_ref.so: the reference's
@@ -66,7 +67,7 @@ def build_problem(idx, O, CF):
     return A, c
 
 
-def run(idx, threads, d, ref=False):
+def run(idx, threads, d, ref=False, sens=False):
     import contextlib
     import oracle as O
     from paper_1605_08771_b200 import configs as CF
@@ -89,7 +90,10 @@ def run(idx, threads, d, ref=False):
     if ref:
         e["library"] = "oracle/_ref/libfeastlab_ref.so (reference sources + oracle/eigen_shim)"
     os.makedirs(os.path.join(GOLD, "parts"), exist_ok=True)
-    with open(os.path.join(GOLD, "parts", f"{'ref' if ref else 'oracle'}_cfg{idx}_{d}.json"), "w") as f:
+    if sens:  # a sensitivity run: outcomes and trace only
+        for k in ("eigenvalues", "residual_norms", "first_filtered"):
+            e.pop(k, None)
+    with open(os.path.join(GOLD, "parts", f"{'sens' if sens else 'ref' if ref else 'oracle'}_cfg{idx}_{d}.json"), "w") as f:
         json.dump({"cfg": idx, "config": c, "driver": d, "result": e}, f)
     print(idx, d, e["iterations"], e["converged"], e["m"], e["recovery_events"], e["seconds"], flush=True)
 
@@ -113,6 +117,14 @@ def merge(idx):
         res = part["result"]
         res.pop("residual_norms", None)  # keep the fixture small: outcomes, trace, eigenvalues
         out["reference_build"][part["driver"]] = res
+    # the same oracle solve with several OpenBLAS threads (a rounding-level
+    # perturbation: only the summation order inside the BLAS changes): where its
+    # trace leaves the one-thread trace the reference algorithm itself is not
+    # reproducible at rounding level (tests/test_gpu_configs.py)
+    out["sensitivity"] = {}
+    for p in sorted(glob.glob(os.path.join(GOLD, "parts", f"sens_cfg{idx}_*.json"))):
+        part = json.load(open(p))
+        out["sensitivity"][part["driver"]] = part["result"]
     with open(os.path.join(GOLD, f"oracle_cfg{idx}.json"), "w") as f:
         json.dump(out, f)
     print("wrote", idx, sorted(out["drivers"]))
@@ -122,4 +134,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "merge":
         merge(int(sys.argv[2]))
     else:
-        run(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], ref=(len(sys.argv) > 4 and sys.argv[4] == "ref"))
+        run(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], ref=(len(sys.argv) > 4 and sys.argv[4] == "ref"),
+            sens=(len(sys.argv) > 4 and sys.argv[4] == "sens"))
