@@ -157,8 +157,11 @@ class ClockSampler:
 # ------------------------------------------------------------------ workload
 def build_workload(cfg_index, device):
     """Seeded synthetic A = Q diag(Lambda) Q^T of the config (fixture, outside
-    the timed region): Lambda from the product's mt19937_64 fills, Q by a
-    device Householder QR (torch.linalg.qr) of the seeded Gaussian block."""
+    the timed region): Lambda from the product's mt19937_64 fills, the seeded
+    Gaussian block filled on the host, Q (blocked Householder QR, sign
+    normalisation) and the assembly by the library's own kernels
+    (fl_fixture_orthogonal / fl_fixture_assemble, proj/src/matmodel.cpp:93-119);
+    torch only owns the device buffer."""
     import torch
 
     import paper_1605_08771_b200 as P
@@ -171,14 +174,8 @@ def build_workload(cfg_index, device):
     if cfg_index == 3:
         A = torch.from_numpy(CF.laplacian_2d()).to(dev)
     else:
-        G = torch.from_numpy(P.gaussian_block(n, n, 1000 + cfg_index)).to(dev)
-        Q, _ = torch.linalg.qr(G)
-        imax = Q.abs().argmax(dim=0)
-        sgn = torch.sign(Q[imax, torch.arange(n, device=dev)])
-        Q = Q * sgn
-        A = (Q * torch.from_numpy(vals).to(dev)) @ Q.T
-        A = 0.5 * (A + A.T)
-        del G, Q
+        A = torch.empty((n, n), dtype=torch.float64, device=dev)
+        P.device_test_matrix(vals, 1000 + cfg_index, A.data_ptr())
     A = A.contiguous()  # row-major storage of a symmetric matrix == column-major
     return A, vals, c
 
@@ -482,18 +479,28 @@ def run_b200(args, rank, world, local_rank):
         return
     mode = P.zgemm_mode()
     zms, zflops, zl = prof["zgemm"]
-    # DRAM bytes per launch of the dominant kernel from the committed ncu
-    # capture of this workload (profiles/), when one exists for it
-    traffic, traffic_src = None, None
-    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                      f"ncu_zgemm_traffic_cfg{args.config}_r01.json")
+    # DRAM bytes per launch of the dominant kernel (the trailing update) from the
+    # committed ncu capture of this workload (profiles/), used only when the
+    # capture ran on the library benched here (sha256 of the .so)
+    traffic, traffic_src, traffic_alg = None, None, None
+    here = os.path.dirname(os.path.abspath(__file__))
+    tp = os.path.join(here, "profiles", f"ncu_zgemm_traffic_cfg{args.config}_r02.json")
     if os.path.exists(tp) and mode == "3m":
+        import hashlib
         with open(tp) as f:
             tj = json.load(f)
-        traffic = round(tj["zgemm_sub"]["dram_bytes_per_launch"])
-        traffic_src = (f"{os.path.relpath(tp, os.path.dirname(os.path.abspath(__file__)))}: "
-                       f"dram__bytes_read.sum + dram__bytes_write.sum per zgemm3m SUB launch "
-                       f"(mean of {tj['zgemm_sub']['launches']})")
+        with open(os.path.join(here, "paper_1605_08771_b200", "lib", "libfeastlab_b200.so"), "rb") as f:
+            digest = hashlib.sha256(f.read()).hexdigest()
+        tu = tj.get("trailing_update")
+        if tu and tj.get("so_sha256") == digest:
+            traffic = round(tu["dram_bytes_per_launch"])
+            traffic_alg = round(tu["algorithmic_bytes"] / tu["launches"])
+            traffic_src = (f"{os.path.relpath(tp, here)}: dram__bytes_read.sum + dram__bytes_write.sum per "
+                           f"{tu['kernel']} launch (mean of {tu['launches']}; measured / algorithmic "
+                           f"{tu['traffic_over_algorithmic']})")
+        else:
+            traffic_src = (f"{os.path.relpath(tp, here)} was captured on another build of the library "
+                           f"(sha256 {str(tj.get('so_sha256'))[:12]} != {digest[:12]}): not used")
     total_ms_prof = sum(v[0] for v in prof.values())
     achieved = zflops / (zms * 1e-3) / 1e12 if zms > 0 else 0.0
     cpu = None
@@ -521,8 +528,9 @@ def run_b200(args, rank, world, local_rank):
         "dtype": "c128/f64 (DMMA m8n8k4 f64)", "data": "synthetic",
         "config": workload_config(args, c, world),
         "fraction_of_fp64_peak": round(value / 1e3 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
-        "roofline": {"kernel": f"zgemm{'3m' if mode == '3m' else ''}_kernel (DMMA; LU trailing "
-                               "update, U12 and blocked solves)",
+        "roofline": {"kernel": ("zgemm3s_kernel (TMA-fed 3M DMMA trailing updates) + zgemm3m_kernel "
+                                "(in-block updates, U12, blocked solves)") if mode == "3m" else
+                               "zgemm_kernel (4M DMMA; LU trailing update, U12 and blocked solves)",
                      "bound": "tensor", "achieved": round(achieved, 3),
                      "product_form": mode,
                      "flop_convention": "algorithmic 8MNK per complex GEMM (both forms); the 3M "
@@ -532,6 +540,7 @@ def run_b200(args, rank, world, local_rank):
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": traffic,
+                     "traffic_algorithmic": traffic_alg,
                      "traffic_source": traffic_src,
                      "peak_source": "measured FP64 DMMA burst, tools/fp64_peak.cu "
                                     "(MEASURED_PEAKS.json has no FP64 entry)",

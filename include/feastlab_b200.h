@@ -283,6 +283,18 @@ int fl_mm_read(const char* path, int* n, double* A, int lda, fl_err* err);
 int fl_mm_write(const char* path, const double* A, int n, int lda, int format, fl_err* err);
 /* seeded column-major N(0,1) / U[lo,hi) fills (fixture generation) */
 void fl_gaussian_fill(double* out, long long count, uint64_t seed);
+/* The orthogonal factor of generate_spectrum (proj/src/matmodel.cpp:93-105) on
+   the device: Householder QR of the n x n block G (column-major, ld n; the
+   seeded Gaussian fill of fl_gaussian_fill), Q = H_1 ... H_n I, every column
+   negated when its largest-magnitude entry is negative. G, Q: FL_HOST or
+   FL_DEVICE memory (loc_g, loc_q); Q has ld n. */
+int fl_fixture_orthogonal(fl_ctx* ctx, const double* G, int n, int loc_g, double* Q, int loc_q,
+                          fl_err* err);
+/* assemble_matrix (proj/src/matmodel.cpp:109-118) on the device:
+   A = 0.5 (M + M^T), M = Q diag(vals) Q^T. Q (ld n) in loc_q memory, vals (n)
+   on the host, A (ld n; may alias Q) in loc_a memory. */
+int fl_fixture_assemble(fl_ctx* ctx, const double* Q, int loc_q, const double* vals, int n,
+                        double* A, int loc_a, fl_err* err);
 void fl_uniform_fill(double* out, long long count, double lo, double hi, uint64_t seed);
 
 #ifdef __cplusplus

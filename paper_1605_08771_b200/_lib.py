@@ -65,6 +65,8 @@ _SIGS = {
     "fl_debug_zgemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
     "fl_debug_zgemm_lu": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
     "fl_debug_factor_tilesums": (_I, [_P, _I, _P]),
+    "fl_fixture_orthogonal": (_I, [_P, _P, _I, _I, _P, _I, _P]),
+    "fl_fixture_assemble": (_I, [_P, _P, _I, _P, _I, _P, _I, _P]),
     "fl_zgemm_mode": (_I, [_I]),
     "fl_solve_many": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P,
                            _P, _P]),

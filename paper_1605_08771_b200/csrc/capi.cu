@@ -1668,6 +1668,62 @@ int fl_debug_factor_tilesums(fl_filter* f, int count, double* out) {
     return cudaStreamSynchronize(ctx->stream) == cudaSuccess ? FL_OK : FL_CUDA;
 }
 
+// ---------------------------------------------------------------- fixtures
+// seeded_orthogonal of proj/src/matmodel.cpp:93-105 on the device: Householder
+// QR of the n x n block G (column-major, ld n), Q = H_1 ... H_n I, columns
+// sign-normalised. G and Q: host or device (loc_*), Q ld n.
+int fl_fixture_orthogonal(fl_ctx* ctx, const double* G, int n, int loc_g, double* Q, int loc_q,
+                          fl_err* err) {
+    return guarded(err, [&] {
+        if (n < 1) throw Fail{FL_INVALID_ARGUMENT, "fl_fixture_orthogonal: need n >= 1"};
+        CtxLock lk(ctx);
+        const int N = round_up(n, FL_TILE);
+        DBuf a, q, v, w, w2, g, t, tau;
+        a.ensure(sizeof(double) * (size_t)N * N);
+        q.ensure(sizeof(double) * (size_t)N * N);
+        v.ensure(sizeof(double) * (size_t)N * FL_TILE);
+        w.ensure(sizeof(double) * (size_t)N * FL_TILE);
+        w2.ensure(sizeof(double) * (size_t)N * FL_TILE);
+        g.ensure(sizeof(double) * FL_TILE * FL_TILE);
+        t.ensure(sizeof(double) * (size_t)N * FL_TILE);
+        tau.ensure(sizeof(double) * N);
+        CK(cudaMemsetAsync(a.p, 0, sizeof(double) * (size_t)N * N, ctx->stream));
+        copy_in(ctx, a.d(), N, n, G, n, n, loc_g);
+        launch_set_diag(a.d(), N, n, N, 1.0, ctx->stream);  // identity padding block
+        if (fixture_householder_q(a.d(), N, q.d(), v.d(), w.d(), w2.d(), g.d(), t.d(), tau.d(),
+                                  ctx->stream) != 0)
+            throw Fail{FL_CUDA, "fl_fixture_orthogonal: launch failed"};
+        fixture_sign_normalize(q.d(), N, n, ctx->stream);
+        g_launch_count += 4 + 10LL * (N / FL_TILE);
+        copy_out(ctx, Q, n, n, q.d(), N, n, loc_q);
+        sync(ctx);
+    });
+}
+
+// assemble_matrix of proj/src/matmodel.cpp:109-118: A = 0.5 (M + M^T),
+// M = Q diag(vals) Q^T. Q (ld n) and A (ld n, may be Q): host or device; vals: host.
+int fl_fixture_assemble(fl_ctx* ctx, const double* Q, int loc_q, const double* vals, int n,
+                        double* A, int loc_a, fl_err* err) {
+    return guarded(err, [&] {
+        if (n < 1) throw Fail{FL_INVALID_ARGUMENT, "fl_fixture_assemble: need n >= 1"};
+        CtxLock lk(ctx);
+        const int N = round_up(n, FL_TILE);
+        DBuf q, b, m, a, vd;
+        q.ensure(sizeof(double) * (size_t)N * N);
+        b.ensure(sizeof(double) * (size_t)N * N);
+        m.ensure(sizeof(double) * (size_t)N * N);
+        a.ensure(sizeof(double) * (size_t)N * N);
+        vd.ensure(sizeof(double) * N);
+        CK(cudaMemsetAsync(q.p, 0, sizeof(double) * (size_t)N * N, ctx->stream));
+        copy_in(ctx, q.d(), N, n, Q, n, n, loc_q);
+        CK(cudaMemcpyAsync(vd.p, vals, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        fixture_assemble(q.d(), vd.d(), N, n, b.d(), m.d(), a.d(), ctx->stream);
+        g_launch_count += 3;
+        copy_out(ctx, A, n, n, a.d(), N, n, loc_a);
+        sync(ctx);
+    });
+}
+
 int fl_ctx_set_reduction(fl_ctx* ctx, int mode) {
     if (!ctx || (mode != FL_REDUCE_SUM && mode != FL_REDUCE_ORDERED)) return FL_INVALID_ARGUMENT;
     CtxLock lk(ctx);

@@ -44,4 +44,11 @@ int launch_qr(double* A, long lda, int n, int p, double* tau, int* jpvt, double*
 int launch_orgqr(const double* A, long lda, const double* tau, int n, int r, double* Q, long ldq,
                  cudaStream_t s);
 
+// Fixture generation on the device (fixture.cu; proj/src/matmodel.cpp:93-119).
+int fixture_householder_q(double* A, int N, double* Q, double* V, double* W, double* W2, double* G,
+                          double* T, double* tau, cudaStream_t s);
+void fixture_sign_normalize(double* Q, long ld, int n, cudaStream_t s);
+void fixture_assemble(const double* Q, const double* vals, int N, int n, double* B, double* M,
+                      double* A, cudaStream_t s);
+
 }  // namespace fl

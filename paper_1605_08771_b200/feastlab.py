@@ -130,7 +130,7 @@ class Context:
     def launches(self) -> int:
         return L.lib().fl_ctx_launches(self.handle)
 
-    KERNEL_CLASSES = ("shift", "panel", "laswp", "trsm", "zgemm", "permute", "accumulate",
+    KERNEL_CLASSES = ("shift", "panel", "laswp", "trsm", "zgemm", "zsum", "permute", "accumulate",
                       "allreduce")
     PHASE_CLASSES = ("eig", "orthonormalize", "rayleigh_ritz")
 
@@ -742,6 +742,49 @@ def gaussian_block(rows: int, cols: int, seed: int) -> np.ndarray:
     out = np.zeros((rows, cols), order="F")
     L.lib().fl_gaussian_fill(_ptr(out), rows * cols, seed)
     return out
+
+
+def seeded_orthogonal(n: int, seed: int, ctx: "Context | None" = None) -> np.ndarray:
+    """The orthogonal factor of generate_spectrum (proj/src/matmodel.cpp:93-105)
+    on the device: blocked Householder QR of the seeded Gaussian block (host
+    fill: a sequential mt19937_64 stream), Q = H_1 ... H_n I, columns
+    sign-normalised."""
+    ctx = ctx or default_context()
+    G = gaussian_block(n, n, seed)
+    Q = np.zeros((n, n), order="F")
+    _call(L.lib().fl_fixture_orthogonal, ctx.handle, _ptr(G), n, L.FL_HOST, _ptr(Q), L.FL_HOST)
+    return Q
+
+
+def assemble_matrix(values, Q, ctx: "Context | None" = None) -> np.ndarray:
+    """assemble_matrix (proj/src/matmodel.cpp:109-118) on the device:
+    0.5 (M + M^T) with M = Q diag(values) Q^T."""
+    ctx = ctx or default_context()
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    Q = np.asfortranarray(Q, dtype=np.float64)
+    n = len(values)
+    if Q.shape != (n, n):
+        raise ValueError("assemble_matrix: inconsistent decomposition")
+    A = np.zeros((n, n), order="F")
+    _call(L.lib().fl_fixture_assemble, ctx.handle, _ptr(Q), L.FL_HOST, _ptr(values), n, _ptr(A),
+          L.FL_HOST)
+    return A
+
+
+def device_test_matrix(values, seed: int, out_ptr: int, ctx: "Context | None" = None) -> None:
+    """The seeded dense test matrix A = Q diag(values) Q^T of the BASELINE
+    configurations, built on the device into the n x n buffer at `out_ptr`
+    (device memory, ld n): Gaussian fill on the host, QR / Q / assembly by the
+    library's kernels (bench.py, large-n tests)."""
+    ctx = ctx or default_context()
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    n = len(values)
+    G = gaussian_block(n, n, seed)
+    _call(L.lib().fl_fixture_orthogonal, ctx.handle, _ptr(G), n, L.FL_HOST, C.c_void_p(out_ptr),
+          L.FL_DEVICE)
+    del G
+    _call(L.lib().fl_fixture_assemble, ctx.handle, C.c_void_p(out_ptr), L.FL_DEVICE, _ptr(values), n,
+          C.c_void_p(out_ptr), L.FL_DEVICE)
 
 
 def uniform_values(count: int, lo: float, hi: float, seed: int) -> np.ndarray:
