@@ -20,7 +20,7 @@
 // Parity pin: the reference cannot be compiled here (Eigen absent), and it
 // ships no golden vectors. This oracle is pinned against every analytic
 // known-answer test and oracle-tolerance test of the reference suite
-// (tests/test_oracle_*.py re-express proj/tests/*.cpp and acceptance.cpp).
+// (tests/test_ref_*.py re-express proj/tests/*.cpp and acceptance.cpp).
 // Bit-level parity with Eigen is unpinned.
 // =============================================================================
 #include <algorithm>

@@ -165,7 +165,8 @@ DeviceBlock initial_block(fl_ctx* ctx, const SymmetricMatrix& A, const SolverCon
 }  // namespace
 
 // drivers.cpp:23-38: mt19937_64(seed ^ golden), N(0,1), column-major; the
-// rank check runs on the device (Gram singular values, threshold 1e-10).
+// rank check is the reference's (ColPivHouseholderQR, threshold 1e-10:
+// drivers.cpp:33-36) on the device (fl_block_rank -> column-pivoted QR).
 MatrixXd make_initial_guess(int n, int m0, std::uint64_t seed) {
     if (m0 < 1 || m0 > n) throw std::invalid_argument("make_initial_guess: require 1 <= m0 <= n");
     std::mt19937_64 gen(seed ^ 0x9e3779b97f4a7c15ULL);
