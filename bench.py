@@ -481,26 +481,25 @@ def run_b200(args, rank, world, local_rank):
     zms, zflops, zl = prof["zgemm"]
     # DRAM bytes per launch of the dominant kernel (the trailing update) from the
     # committed ncu capture of this workload (profiles/), used only when the
-    # capture ran on the library benched here (sha256 of the .so)
+    # capture ran on the library sources benched here (sha256 over csrc/ and include/)
     traffic, traffic_src, traffic_alg = None, None, None
     here = os.path.dirname(os.path.abspath(__file__))
     tp = os.path.join(here, "profiles", f"ncu_zgemm_traffic_cfg{args.config}_r02.json")
     if os.path.exists(tp) and mode == "3m":
-        import hashlib
+        from paper_1605_08771_b200._lib import source_digest
         with open(tp) as f:
             tj = json.load(f)
-        with open(os.path.join(here, "paper_1605_08771_b200", "lib", "libfeastlab_b200.so"), "rb") as f:
-            digest = hashlib.sha256(f.read()).hexdigest()
+        digest = source_digest()
         tu = tj.get("trailing_update")
-        if tu and tj.get("so_sha256") == digest:
+        if tu and tj.get("src_sha256") == digest:
             traffic = round(tu["dram_bytes_per_launch"])
             traffic_alg = round(tu["algorithmic_bytes"] / tu["launches"])
             traffic_src = (f"{os.path.relpath(tp, here)}: dram__bytes_read.sum + dram__bytes_write.sum per "
                            f"{tu['kernel']} launch (mean of {tu['launches']}; measured / algorithmic "
                            f"{tu['traffic_over_algorithmic']})")
         else:
-            traffic_src = (f"{os.path.relpath(tp, here)} was captured on another build of the library "
-                           f"(sha256 {str(tj.get('so_sha256'))[:12]} != {digest[:12]}): not used")
+            traffic_src = (f"{os.path.relpath(tp, here)} was captured on other sources of the library "
+                           f"(sha256 {str(tj.get('src_sha256'))[:12]} != {digest[:12]}): not used")
     total_ms_prof = sum(v[0] for v in prof.values())
     achieved = zflops / (zms * 1e-3) / 1e12 if zms > 0 else 0.0
     cpu = None

@@ -130,3 +130,23 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def source_digest() -> str:
+    """sha256 over the library's sources (csrc/**, the public headers): ties a
+    committed profile capture to the code it ran (the built .so is not
+    bit-reproducible across builds, so its own hash cannot)."""
+    import hashlib
+    here = os.path.dirname(os.path.abspath(__file__))
+    roots = [os.path.join(here, "csrc"), os.path.join(os.path.dirname(here), "include")]
+    files = []
+    for r in roots:
+        for d, _, names in os.walk(r):
+            files += [os.path.join(d, n) for n in names
+                      if n.endswith((".cu", ".cuh", ".hpp", ".h", ".cpp")) or n == "Makefile"]
+    h = hashlib.sha256()
+    for f in sorted(files):
+        h.update(os.path.relpath(f, os.path.dirname(here)).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()

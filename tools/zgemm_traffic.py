@@ -4,8 +4,8 @@ metrics pass, against their algorithmic bytes:
       --clock-control none -k regex:zgemm --csv --log-file gpurun_out/zt.csv \
       python tools/one_app.py 4 lu 1
   python tools/zgemm_traffic.py gpurun_out/zt.csv 4 > profiles/ncu_zgemm_traffic_cfg4_r02.json
-The JSON records the sha256 of the library the capture ran on; bench.py uses
-the figure only when that digest is the benched library's."""
+The JSON records the sha256 of the library's sources the capture ran on;
+bench.py uses the figure only when that digest is the benched sources'."""
 import collections
 import csv
 import hashlib
@@ -18,9 +18,7 @@ sys.path.insert(0, ROOT)
 from paper_1605_08771_b200 import configs as CF  # noqa: E402
 
 
-def so_digest():
-    with open(os.path.join(ROOT, "paper_1605_08771_b200", "lib", "libfeastlab_b200.so"), "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()
+from paper_1605_08771_b200._lib import source_digest  # noqa: E402
 
 
 def trailing_algorithmic_bytes(N, nodes, kb):
@@ -62,7 +60,7 @@ def main(path, cfg):
     calg, oalg = trailing_algorithmic_bytes(N, c.n_c, kb)
     out = {"source": f"{path}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum of one "
                      f"cfg{cfg} LU filter application (node chunks on one stream)",
-           "so_sha256": so_digest(), "cfg": cfg, "kernels": {}}
+           "src_sha256": source_digest(), "cfg": cfg, "kernels": {}}
     for name, m in per.items():
         n = len(ids[name])
         rd, wr = m.get("dram__bytes_read.sum", 0.0), m.get("dram__bytes_write.sum", 0.0)
