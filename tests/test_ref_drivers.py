@@ -1,5 +1,5 @@
 """Re-expresses proj/tests/test_drivers.cpp, test_matmodel.cpp and
-acceptance C4/C5/C7/C8/C9/C10 (proj/tests/acceptance.cpp) against both the CPU oracle (pin) and the B200 path (F = b200, -m gpu)."""
+acceptance C4/C5/C6/C7/C8/C9/C10 (proj/tests/acceptance.cpp) against both the CPU oracle (pin) and the B200 path (F = b200, -m gpu)."""
 import numpy as np
 import pytest
 
@@ -231,6 +231,37 @@ def test_acceptance_c5_contrast(F):
         sol = d(dense, KBENCH, F.SolverConfig(m0=51, n_c=8, s=3, tol=1e-6, max_iter=25,
                                               cache_factorizations=True))
         assert sol.converged
+
+
+@pytest.mark.slow
+def test_acceptance_c6_rhs_cost(F):
+    """acceptance.cpp:248-291: on the dense benchmark family the accelerated
+    drivers reach a max residual of 1e-6 with at most half the right-hand-side
+    solves of the best plain-FEAST cell of the (m0, n_c) grid."""
+    dense = _benchmark_family(True)
+    target = 1e-6
+
+    def rhs_to_target(sol):
+        for rec in sol.trace:
+            if rec.max_residual <= target:
+                return rec.rhs_cumulative
+        return -1  # never reached
+
+    best_feast = -1
+    for m0 in (51, 75, 102):
+        for nc in (3, 8):
+            sol = F.feast_solve(dense, KBENCH, F.SolverConfig(m0=m0, n_c=nc, tol=target, max_iter=40,
+                                                              cache_factorizations=True))
+            rhs = rhs_to_target(sol)
+            if rhs >= 0 and (best_feast < 0 or rhs < best_feast):
+                best_feast = rhs
+    for d in (F.xfeast_solve, F.rfeast_solve):
+        sol = d(dense, KBENCH, F.SolverConfig(m0=51, n_c=8, s=3, tol=target, max_iter=40,
+                                              cache_factorizations=True))
+        rhs = rhs_to_target(sol)
+        assert rhs >= 0, "accelerated driver never reached 1e-6"
+        if best_feast >= 0:  # best_feast < 0: no feast cell reached the target at all
+            assert 2 * rhs <= best_feast, (rhs, best_feast)
 
 
 def test_acceptance_c7_clustered(F):
