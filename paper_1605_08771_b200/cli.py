@@ -74,8 +74,9 @@ def build_parser() -> argparse.ArgumentParser:
     return ap
 
 
-def run_solve(opt, out=sys.stdout) -> int:  # feastlab_cli.cpp:137-187
+def run_solve(opt, out=None) -> int:  # feastlab_cli.cpp:137-187
     from . import feastlab as P
+    out = out or sys.stdout
     cfg = P.SolverConfig(m0=opt.m0, n_c=opt.nc, s=opt.s, tol=opt.tol, max_iter=opt.max_iter,
                          seed=opt.seed, orthogonalizer=opt.orthogonalizer,
                          cache_factorizations=opt.cache_factorizations)
