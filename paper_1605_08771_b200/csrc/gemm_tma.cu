@@ -174,6 +174,10 @@ __global__ void __launch_bounds__(128, 2)
     // compiler memory barriers. Tile kt + LEAD reuses the stage of tile kt - 1,
     // which the other warps have left by the middle of tile kt: the producer
     // thread issues it there and rarely blocks.
+    // unrolled by the ring depth: stage addresses, barrier addresses and the
+    // producing warp become compile-time per copy (0.937 -> 0.954 of the DMMA
+    // issue peak; a CTA alone on its SM 0.72 -> 0.76)
+#pragma unroll 4
     for (int kt = 0; kt < KT; ++kt) {
         const int s = kt % TS;
         if (kt == kt_c) prefetch_c();
