@@ -134,8 +134,8 @@ def _first_difference(ta, tb):
 
 # The reference algorithm's XFEAST / RFEAST (and stagnating FEAST) trajectories
 # are not reproducible at rounding level by the reference algorithm itself: the
-# oracle run with 6 OpenBLAS threads instead of 1 (only the summation order
-# inside the BLAS changes) leaves the one-thread trace after a few iterations
+# oracle run with 2, 3, 4 or 6 OpenBLAS threads instead of 1 (only the summation
+# order inside the BLAS changes) leaves the one-thread trace after a few iterations
 # and ends with other iteration / converged counts (cfg0 XFEAST 16 -> 13
 # iterations, cfg1 XFEAST 10 converged -> 20 not converged; goldens'
 # "sensitivity"). The decisions that flip are the Gram-floor rank (eigenvalues
@@ -182,13 +182,17 @@ def test_drivers_vs_golden_oracle(index, driver, cfg0):
     if k_gpu is not None and k_gpu < min(len(tr), len(gtr)):
         print(f"  first differing record: gpu {tr[k_gpu]} oracle {gtr[k_gpu]} "
               f"(oracle max residual / tol there {gold['trace'][k_gpu][3] / c['tol']:.3e})")
-    sens = gold_all.get("sensitivity", {}).get(driver)
-    horizon = None
-    if sens is not None:
+    sens_runs = gold_all.get("sensitivity", {}).get(driver) or []
+    if isinstance(sens_runs, dict):
+        sens_runs = [sens_runs]
+    horizon = None  # the earliest record at which any perturbed oracle run leaves the golden trace
+    for sens in sens_runs:
         strace = [[t[0], t[1], t[2], t[4]] for t in sens["trace"]]
-        horizon = _first_difference(gtr, strace)
+        h = _first_difference(gtr, strace)
         print(f"  oracle with {sens['oracle_threads']} threads: {sens['iterations']} it conv={sens['converged']} "
-              f"m={sens['m']}; leaves the one-thread trace at record {horizon}")
+              f"m={sens['m']}; leaves the one-thread trace at record {h}")
+        if h is not None:
+            horizon = h if horizon is None else min(horizon, h)
     scale = max(np.abs(vals).max(), 1.0)
     stagnating_feast = driver == "feast_solve" and not gold["converged"]
     if horizon is None and not stagnating_feast:

@@ -93,7 +93,8 @@ def run(idx, threads, d, ref=False, sens=False):
     if sens:  # a sensitivity run: outcomes and trace only
         for k in ("eigenvalues", "residual_norms", "first_filtered"):
             e.pop(k, None)
-    with open(os.path.join(GOLD, "parts", f"{'sens' if sens else 'ref' if ref else 'oracle'}_cfg{idx}_{d}.json"), "w") as f:
+    tag = f"sens_cfg{idx}_{d}_t{threads}" if sens else f"{'ref' if ref else 'oracle'}_cfg{idx}_{d}"
+    with open(os.path.join(GOLD, "parts", tag + ".json"), "w") as f:
         json.dump({"cfg": idx, "config": c, "driver": d, "result": e}, f)
     print(idx, d, e["iterations"], e["converged"], e["m"], e["recovery_events"], e["seconds"], flush=True)
 
@@ -117,14 +118,14 @@ def merge(idx):
         res = part["result"]
         res.pop("residual_norms", None)  # keep the fixture small: outcomes, trace, eigenvalues
         out["reference_build"][part["driver"]] = res
-    # the same oracle solve with several OpenBLAS threads (a rounding-level
+    # the same oracle solve with 2 ... 8 OpenBLAS threads, one run each (a rounding-level
     # perturbation: only the summation order inside the BLAS changes): where its
     # trace leaves the one-thread trace the reference algorithm itself is not
     # reproducible at rounding level (tests/test_gpu_configs.py)
     out["sensitivity"] = {}
     for p in sorted(glob.glob(os.path.join(GOLD, "parts", f"sens_cfg{idx}_*.json"))):
         part = json.load(open(p))
-        out["sensitivity"][part["driver"]] = part["result"]
+        out["sensitivity"].setdefault(part["driver"], []).append(part["result"])
     with open(os.path.join(GOLD, f"oracle_cfg{idx}.json"), "w") as f:
         json.dump(out, f)
     print("wrote", idx, sorted(out["drivers"]))
