@@ -141,6 +141,10 @@ int fl_debug_zgemm_lu(fl_ctx* ctx, int N, int M, int Nc, int K, int batch, int i
 /* weighted sums of the 64 x 64 tiles of the factors in slots [0, count)
    (instrumentation: compares factorizations across runs) */
 int fl_debug_factor_tilesums(fl_filter* f, int count, double* out);
+/* on != 0: the drivers' rounding-sensitive decisions (Gram-floor rank of
+   orthonormalize, inside test of rayleigh_ritz) are written to stderr with their
+   margins; on < 0 only queries. Returns the setting (instrumentation). */
+int fl_debug_decision_log(int on);
 /* cycle counts of the LU panel kernel's phases (instrumentation) */
 int fl_debug_panel_profile(double* out8, int reset);
 /* per-warp clock64 trace of the first on-chip panel (builds with FL_PANEL_TRACE) */

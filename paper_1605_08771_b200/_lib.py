@@ -67,6 +67,7 @@ _SIGS = {
     "fl_debug_factor_tilesums": (_I, [_P, _I, _P]),
     "fl_fixture_orthogonal": (_I, [_P, _P, _I, _I, _P, _I, _P]),
     "fl_fixture_assemble": (_I, [_P, _P, _I, _P, _I, _P, _I, _P]),
+    "fl_debug_decision_log": (_I, [_I]),
     "fl_zgemm_mode": (_I, [_I]),
     "fl_solve_many": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P,
                            _P, _P]),

@@ -25,6 +25,9 @@
 namespace fl {
 std::atomic<long long> g_launch_count{0};
 }
+// fl_debug_decision_log: the rounding-sensitive decisions of the drivers are
+// written to stderr with their margins (tests/test_gpu_configs.py reads them)
+static std::atomic<int> g_decision_log{0};
 
 namespace {
 
@@ -1159,6 +1162,21 @@ void orthonormalize_dev(fl_ctx* ctx, const fl_block* X, double drop_tol, fl_bloc
     for (int i = p - 1; i >= 0; --i)
         if (ev[i] > ev_floor) keep.push_back(i);
     const int rank = (int)keep.size();
+    if (g_decision_log.load()) {
+        // the Gram-floor rank decision (ritz.cpp:44-49): the kept and dropped
+        // eigenvalues next to the floor, and the eigensolver's absolute error
+        // scale eps * ev_max, all relative to the floor
+        const double eps = std::numeric_limits<double>::epsilon();
+        const double kept_min = rank > 0 ? ev[p - rank] : 0.0;
+        const double drop_max = rank < p ? ev[p - rank - 1] : 0.0;
+        int near = 0;  // eigenvalues within 8 eps ev_max of the floor: undecidable
+        for (int i = 0; i < p; ++i)
+            if (std::abs(ev[i] - ev_floor) <= 8.0 * eps * ev[p - 1]) ++near;
+        std::fprintf(stderr,
+                     "decision gram_floor p=%d rank=%d kept_min/floor=%.6f dropped_max/floor=%.6f "
+                     "eps*ev_max/floor=%.3e within_8eps=%d\n",
+                     p, rank, kept_min / ev_floor, drop_max / ev_floor, eps * ev[p - 1] / ev_floor, near);
+    }
     if (rank == 0) throw Fail{FL_RUNTIME_ERROR, "orthonormalize: block is numerically zero"};
     const int RP = round_up(rank, FL_TILE);
     // Vk = V[:, keep] (zero padded), U = X Vk, U[:, j] /= sigma_j (:53-57)
@@ -1280,6 +1298,22 @@ void rayleigh_ritz_dev(fl_ctx* ctx, const fl_matrix* A, const fl_block* X, doubl
     CK(cudaMemcpyAsync(out.norms.data(), nrm, sizeof(double) * p, cudaMemcpyDeviceToHost, s));
     sync(ctx);
     for (int k = 0; k < p; ++k) out.inside[k] = (out.vals[k] > lo && out.vals[k] < hi) ? 1 : 0;
+    if (g_decision_log.load()) {
+        // the inside test (ritz.cpp:108-112): the Ritz value nearest to an interval
+        // edge, relative to the interval's half width, and that pair's residual
+        double best = 1e300, res = 0.0;
+        int m = 0;
+        for (int k = 0; k < p; ++k) {
+            m += out.inside[k];
+            const double d = std::min(std::abs(out.vals[k] - lo), std::abs(out.vals[k] - hi));
+            if (d < best) {
+                best = d;
+                res = out.norms[k];
+            }
+        }
+        std::fprintf(stderr, "decision inside p=%d m=%d nearest_edge_distance/radius=%.3e its_residual=%.3e\n",
+                     p, m, best / (0.5 * (hi - lo)), res);
+    }
 }
 
 template <class F>
@@ -1722,6 +1756,11 @@ int fl_fixture_assemble(fl_ctx* ctx, const double* Q, int loc_q, const double* v
         copy_out(ctx, A, n, n, a.d(), N, n, loc_a);
         sync(ctx);
     });
+}
+
+int fl_debug_decision_log(int on) {
+    if (on >= 0) g_decision_log.store(on ? 1 : 0);
+    return g_decision_log.load();
 }
 
 int fl_ctx_set_reduction(fl_ctx* ctx, int mode) {

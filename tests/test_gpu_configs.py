@@ -150,7 +150,7 @@ HORIZON_SLACK = 3
 
 @pytest.mark.parametrize("driver", ["feast_solve", "xfeast_solve", "rfeast_solve"])
 @pytest.mark.parametrize("index", [0, 1, 2, 3, 4])
-def test_drivers_vs_golden_oracle(index, driver, cfg0):
+def test_drivers_vs_golden_oracle(index, driver, cfg0, capfd):
     """North-star gate: identical iteration counts, converged counts, traces
     (iter, subspace_dim, rhs_cumulative, m_found) and recovery events, against
     the one-thread oracle goldens (the reference is built single-threaded,
@@ -172,7 +172,14 @@ def test_drivers_vs_golden_oracle(index, driver, cfg0):
     gold = drivers[driver]
     A, vals, Q, c = cfg0 if index == 0 else _fixture(index)
     cfg = P.SolverConfig(m0=c["m0"], n_c=c["n_c"], tol=c["tol"], max_iter=c["max_iter"], s=c["s"])
-    sol = getattr(P, driver)(A, P.SearchInterval(c["lo"], c["hi"]), cfg)
+    from paper_1605_08771_b200 import _lib
+    capfd.readouterr()
+    _lib.lib().fl_debug_decision_log(1)  # margins of the rounding-sensitive decisions -> stderr
+    try:
+        sol = getattr(P, driver)(A, P.SearchInterval(c["lo"], c["hi"]), cfg)
+    finally:
+        _lib.lib().fl_debug_decision_log(0)
+    decisions = [l for l in capfd.readouterr().err.splitlines() if l.startswith("decision ")]
     tr = _trace(sol)
     gtr = [[t[0], t[1], t[2], t[4]] for t in gold["trace"]]
     print(f"cfg{index} {driver}: gpu {sol.iterations} it conv={sol.converged} m={len(sol.eigenvalues)} "
@@ -182,6 +189,22 @@ def test_drivers_vs_golden_oracle(index, driver, cfg0):
     if k_gpu is not None and k_gpu < min(len(tr), len(gtr)):
         print(f"  first differing record: gpu {tr[k_gpu]} oracle {gtr[k_gpu]} "
               f"(oracle max residual / tol there {gold['trace'][k_gpu][3] / c['tol']:.3e})")
+    if k_gpu is not None:
+        # the B200 side's margins: Gram eigenvalues next to the eps * p * max floor
+        # (their absolute error is of order eps * max, i.e. 1 / p of the floor) and
+        # Ritz values next to an interval edge
+        def margin(line):
+            f = dict(kv.split("=") for kv in line.split()[2:])
+            return min(abs(float(f["kept_min/floor"]) - 1.0), abs(1.0 - float(f["dropped_max/floor"])))
+        gram = [l for l in decisions if l.startswith("decision gram_floor")]
+        close = sorted(gram, key=margin)[:3]
+        print(f"  {len(gram)} Gram-floor rank decisions on the B200 path; the three closest to the floor:")
+        for l in close:
+            print("    " + l[len("decision gram_floor "):])
+        edge = [l for l in decisions if l.startswith("decision inside")]
+        if edge:
+            nearest = min(edge, key=lambda l: float(l.split("nearest_edge_distance/radius=")[1].split()[0]))
+            print("  Ritz value nearest to an interval edge: " + nearest[len("decision inside "):])
     sens_runs = gold_all.get("sensitivity", {}).get(driver) or []
     if isinstance(sens_runs, dict):
         sens_runs = [sens_runs]
