@@ -99,13 +99,13 @@ def test_ldlt_first_filtered_vs_golden(ldlt, index):
                                           (0, "rfeast_solve"), (1, "feast_solve"),
                                           (1, "xfeast_solve"), (1, "rfeast_solve"),
                                           (3, "feast_solve")])
-def test_ldlt_drivers_vs_golden(ldlt, index, driver):
+def test_ldlt_drivers_vs_golden(ldlt, index, driver, capfd):
     """Drivers on the LDL^T filter: the golden oracle's iteration / converged
     counts, traces and eigenvalues (the same gates as test_gpu_configs)."""
     import test_gpu_configs as TC
     P = ldlt
     try:
-        TC.test_drivers_vs_golden_oracle(index, driver, TC._fixture(0))
+        TC.test_drivers_vs_golden_oracle(index, driver, TC._fixture(0), capfd)
     except P.FeastRuntimeError as e:
         # cfg1 FEAST stagnates in the reference algorithm (not converged after 20
         # iterations on the oracle): with the LDL^T filter's rounding the same
