@@ -145,7 +145,7 @@ def _first_difference(ta, tb):
 # implementation, the reference's included; up to it the B200 trace must be
 # the oracle's. The horizon is taken HORIZON_SLACK records early, since the
 # rounding event that makes two runs part precedes the first record that shows it.
-HORIZON_SLACK = 3
+HORIZON_SLACK = 2
 
 
 @pytest.mark.parametrize("driver", ["feast_solve", "xfeast_solve", "rfeast_solve"])
