@@ -186,6 +186,8 @@ struct fl_filter {
     int kb = 0, ke = 0;  // local node range [kb, ke)
     // factors: cache -> one per local node; else a rotating group
     DBuf fac_re, fac_im, ipiv, perm, bad, ptab;
+    DBuf cmap, btab;             // composed outer-block interchanges (launch_laswp_block)
+    int laswp_block = 1;         // FEASTLAB_LASWP_BLOCK=0: one interchange pass per panel
     DBuf inv_re, inv_im;  // per slot: NB inverted L_ii blocks, then NB inverted U_ii blocks
     DBuf lt_re, lt_im;    // LDL^T: per slot, the current panel's L_kk^{-T} (64 x 64)
     // TMA-fed trailing updates (gemm_tma.cu): per slot the sum planes Re + Im of
@@ -214,13 +216,14 @@ struct fl_filter {
         int p, slots, ns, zmode, reduction, factorization;
         int phase;  // 0: factor + solve (no cache); cache: 1 factor + solve, 2 solve only
         int lu_panels, solve_panels, panel_res_rows;  // blocking (environment-tunable)
+        int laswp_block;
         bool operator==(const GraphKey& o) const {
             return X == o.X && Y == o.Y && fac == o.fac && w == o.w && ldx == o.ldx &&
                    ldy == o.ldy && p == o.p && slots == o.slots && ns == o.ns &&
                    zmode == o.zmode && reduction == o.reduction &&
                    factorization == o.factorization && phase == o.phase &&
                    lu_panels == o.lu_panels && solve_panels == o.solve_panels &&
-                   panel_res_rows == o.panel_res_rows;
+                   panel_res_rows == o.panel_res_rows && laswp_block == o.laswp_block;
         }
     };
     GraphKey gkey{}, gseen{};
@@ -383,6 +386,12 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
     }
     int* ipiv = f->ipiv.i() + (long)s0 * N;
     int* ptab = f->ptab.i() + (long)s0 * (4 * FL_TILE + 1);
+    int* cmap = f->cmap.i() + (long)s0 * N;
+    int* btab = f->btab.i() + (long)s0 * LB_TAB;
+    if (f->laswp_block) {
+        Prof pr(ctx, P_LASWP, 0.0, 1, st);
+        launch_perm_identity(cmap, N, G, st);
+    }
     const int NB = N / FL_TILE;
     const long istride = 2L * NB * FL_TILE * FL_TILE;
     ZBatch Inv{f->inv_re.d() + s0 * istride, f->inv_im.d() + s0 * istride, FL_TILE, istride};
@@ -483,11 +492,23 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
         CK(cudaEventRecord(ev_panel, sp));
         CK(cudaStreamWaitEvent(st, ev_panel, 0));
         const int rest = N - c0;
-        for (int j = 0; j < np; ++j) {
-            // panels 1..np-2 already swapped the block's columns left of them (sp)
-            const int left = j == np - 1 ? k0 + j * T : k0;
-            if (rest > 0) swaps(tabs[j], 0, left, c0, N, st);
-            else swaps(tabs[j], 0, left, 0, 0, st);
+        if (f->laswp_block && np >= 2) {
+            // the columns outside the block take the composition of the block's
+            // np net permutations in one pass; the block's own columns left of
+            // its last panel still lack that panel's interchanges
+            {
+                Prof pr(ctx, P_LASWP, 0.0, 2, st);
+                launch_laswp_block(F, N, k0, np, 0, k0, c0, N, tabs[0],
+                                   (long)f->fac_slots * (4 * T + 1), cmap, btab, G, st);
+            }
+            swaps(tabs[np - 1], k0, k0 + (np - 1) * T, 0, 0, st);
+        } else {
+            for (int j = 0; j < np; ++j) {
+                // panels 1..np-2 already swapped the block's columns left of them (sp)
+                const int left = j == np - 1 ? k0 + j * T : k0;
+                if (rest > 0) swaps(tabs[j], 0, left, c0, N, st);
+                else swaps(tabs[j], 0, left, 0, 0, st);
+            }
         }
         if (rest <= 0) break;
         for (int j = 0; j < np; ++j) {
@@ -785,6 +806,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
         f->ipiv.ensure(sizeof(int) * (size_t)N * slots);
         f->perm.ensure(sizeof(int) * (size_t)N * slots);
         f->ptab.ensure(sizeof(int) * (size_t)(4 * FL_TILE + 1) * FL_MAX_BLOCK_PANELS * slots);
+        f->cmap.ensure(sizeof(int) * (size_t)N * slots);
+        f->btab.ensure(sizeof(int) * (size_t)LB_TAB * slots);
         f->inv_re.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->inv_im.ensure(sizeof(double) * 2 * (size_t)N * FL_TILE * slots);
         f->lt_re.ensure(sizeof(double) * (size_t)FL_TILE * FL_TILE * slots);
@@ -812,6 +835,10 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
                                  N >= 12288 ? (L >= 8 ? 16 : 8) : (L >= 8 ? 4 : 2),
                                  FL_MAX_BLOCK_PANELS);
     f->solve_panels = block_panels("FEASTLAB_SOLVE_PANELS", 4, 8);
+    {
+        const char* e = std::getenv("FEASTLAB_LASWP_BLOCK");
+        f->laswp_block = !(e && e[0] == '0');
+    }
     // sum planes and tensor maps of the TMA-fed trailing updates (outer blocks
     // of at least 128 columns, 3M product)
     if (tma_updates() && f->lu_panels >= 2 &&
@@ -964,7 +991,8 @@ void filter_apply_dev(fl_filter* f, const double* X, long ldx, int p, double* Y,
     const int phase = f->cache ? (needs_factor ? 1 : 2) : 0;
     const fl_filter::GraphKey key{X, Y, f->fac_re.p, f->w_re.p, ldx, ldy, p, slots, ns,
                                   zgemm_mode(), ctx->reduction, ctx->factorization, phase,
-                                  f->lu_panels, f->solve_panels, f->panel_res_rows};
+                                  f->lu_panels, f->solve_panels, f->panel_res_rows,
+                                  f->laswp_block};
     const bool graphable = !ctx->prof.on && graphs_enabled();
     const bool big = N >= 2048;
     if (graphable && f->gexec && f->gkey == key && phase != 1) {

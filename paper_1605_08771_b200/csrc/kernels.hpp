@@ -122,6 +122,17 @@ int res_panel_trace(long long* out, int max);
 // Apply a panel's 64 row interchanges (ptab) to the columns [a0,a1) U [b0,b1).
 void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int batch,
                   cudaStream_t s);
+// Outer-block form: the composition of the np panel tables of the outer block
+// at k0 (tables ptab + j * panel_stride, j < np <= 16) applied in one pass to
+// the columns [a0,a1) U [b0,b1), both outside the block. cmap: N ints per node,
+// identity on entry and on exit (launch_perm_identity); btab: LB_TAB ints per
+// node of scratch.
+constexpr int LB_MAX = 16 * 64;  // rows of the widest outer block
+constexpr int LB_TAB = 1 + 3 * LB_MAX;
+void launch_perm_identity(int* cmap, int N, int batch, cudaStream_t s);
+void launch_laswp_block(ZBatch F, int N, int k0, int np, int a0, int a1, int b0, int b1,
+                        const int* ptab, long panel_stride, int* cmap, int* btab, int batch,
+                        cudaStream_t s);
 // Inverses of `nblocks` consecutive 64x64 diagonal blocks starting at (r0, r0):
 // unit-lower (upper=false) or upper. Block j of node b is stored at
 // Inv.re/im + b*Inv.stride + (first_block + j)*4096, column-major ld 64.

@@ -197,6 +197,138 @@ void launch_laswp(ZBatch F, int a0, int a1, int b0, int b1, const int* ptab, int
                                                                                   b1, ptab);
 }
 
+// ------------------------------------------------------------------ outer-block laswp
+// The np panels of an outer block leave np net permutations; the columns
+// outside the block need only their composition, applied in ONE pass: the
+// block's own bw = 64 np rows are then written as whole lines (no sector fill
+// for a partial write), and each displaced row below the block is read and
+// written once instead of once per panel that touched it.
+//
+// compose_perm_kernel: cmap[r] = the row whose data sits at position r (identity
+// on entry and on exit); a panel table moves cmap[src] to pos. Table written
+// per node: [0] count of moved rows below the block, then the source row of
+// each of the block's rows, then (position, source) of the moved rows below.
+__global__ void __launch_bounds__(128) compose_perm_kernel(const int* __restrict__ ptab,
+                                                           long panel_stride, int np, int k0,
+                                                           int N, int* cmap_all, int* btab_all) {
+    const int b = blockIdx.x, t = threadIdx.x;
+    int* cmap = cmap_all + (long)b * N;
+    int* out = btab_all + (long)b * LB_TAB;
+    __shared__ int rc;
+    if (t == 0) rc = 0;
+    for (int j = 0; j < np; ++j) {
+        const int* tab = ptab + j * panel_stride + (long)b * (4 * PW + 1);
+        const int cnt = tab[0];
+        int v = 0;
+        if (t < cnt) v = cmap[tab[1 + 2 * PW + t]];
+        __syncthreads();
+        if (t < cnt) cmap[tab[1 + t]] = v;
+        __syncthreads();
+    }
+    const int bw = np * PW, c0 = k0 + bw;
+    for (int i = t; i < bw; i += blockDim.x) {
+        out[1 + i] = cmap[k0 + i];
+        cmap[k0 + i] = k0 + i;
+    }
+    for (int j = 0; j < np; ++j) {
+        const int* tab = ptab + j * panel_stride + (long)b * (4 * PW + 1);
+        const int cnt = tab[0];
+        if (t < cnt) {
+            const int p = tab[1 + t];
+            if (p >= c0) {
+                const int v = atomicExch(&cmap[p], p);  // first claim lists it, and resets
+                if (v != p) {
+                    const int s = atomicAdd(&rc, 1);
+                    out[1 + LB_MAX + s] = p;
+                    out[1 + 2 * LB_MAX + s] = v;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (t == 0) out[0] = rc;
+}
+
+__global__ void iota_kernel(int* a, long n, int period) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int)(i % period);
+}
+
+// LB_CW columns per CTA; thread t owns block rows t + 256 q and moved rows
+// t + 256 q below the block. Every load of the CTA is issued before the barrier,
+// every store after it (a column's sources and positions overlap).
+constexpr int LB_CW = 2, LB_Q = LB_MAX / 256;
+__global__ void __launch_bounds__(256) laswp_block_kernel(ZBatch F, int k0, int bw, int a0,
+                                                          int a1, int b0, int b1,
+                                                          const int* __restrict__ btab) {
+    const int b = blockIdx.y, t = threadIdx.x;
+    const int* tab = btab + (long)b * LB_TAB;
+    const int rc = __ldg(tab);
+    int ds[LB_Q], rp[LB_Q], rs[LB_Q];
+#pragma unroll
+    for (int q = 0; q < LB_Q; ++q) {
+        const int i = t + 256 * q;
+        ds[q] = i < bw ? __ldg(tab + 1 + i) : -1;
+        if (ds[q] == k0 + i) ds[q] = -1;  // stays
+        rp[q] = i < rc ? __ldg(tab + 1 + LB_MAX + i) : -1;
+        rs[q] = i < rc ? __ldg(tab + 1 + 2 * LB_MAX + i) : -1;
+    }
+    const int na = a1 - a0, ncols = na + (b1 - b0);
+    double* Fr = F.re + b * F.stride;
+    double* Fi = F.im + b * F.stride;
+    long cb[LB_CW];
+#pragma unroll
+    for (int w = 0; w < LB_CW; ++w) {
+        const int k = blockIdx.x * LB_CW + w;
+        cb[w] = k < ncols ? (long)(k < na ? a0 + k : b0 + (k - na)) * F.ld : -1;
+    }
+    double dr[LB_CW][LB_Q], di[LB_CW][LB_Q], vr[LB_CW][LB_Q], vi[LB_CW][LB_Q];
+#pragma unroll
+    for (int w = 0; w < LB_CW; ++w)
+#pragma unroll
+        for (int q = 0; q < LB_Q; ++q) {
+            if (cb[w] >= 0 && ds[q] >= 0) {
+                dr[w][q] = Fr[cb[w] + ds[q]];
+                di[w][q] = Fi[cb[w] + ds[q]];
+            }
+            if (cb[w] >= 0 && rs[q] >= 0) {
+                vr[w][q] = Fr[cb[w] + rs[q]];
+                vi[w][q] = Fi[cb[w] + rs[q]];
+            }
+        }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < LB_CW; ++w)
+#pragma unroll
+        for (int q = 0; q < LB_Q; ++q) {
+            if (cb[w] >= 0 && ds[q] >= 0) {
+                Fr[cb[w] + k0 + t + 256 * q] = dr[w][q];
+                Fi[cb[w] + k0 + t + 256 * q] = di[w][q];
+            }
+            if (cb[w] >= 0 && rs[q] >= 0) {
+                Fr[cb[w] + rp[q]] = vr[w][q];
+                Fi[cb[w] + rp[q]] = vi[w][q];
+            }
+        }
+}
+
+void launch_perm_identity(int* cmap, int N, int batch, cudaStream_t s) {
+    const long n = (long)N * batch;
+    iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cmap, n, N);
+}
+
+void launch_laswp_block(ZBatch F, int N, int k0, int np, int a0, int a1, int b0, int b1,
+                        const int* ptab, long panel_stride, int* cmap, int* btab, int batch,
+                        cudaStream_t s) {
+    a1 = a1 > a0 ? a1 : a0;
+    b1 = b1 > b0 ? b1 : b0;
+    const int ncols = (a1 - a0) + (b1 - b0);
+    if (ncols <= 0 || np <= 0) return;
+    compose_perm_kernel<<<batch, 128, 0, s>>>(ptab, panel_stride, np, k0, N, cmap, btab);
+    laswp_block_kernel<<<dim3((ncols + LB_CW - 1) / LB_CW, batch), 256, 0, s>>>(
+        F, k0, np * PW, a0, a1, b0, b1, btab);
+}
+
 // ------------------------------------------------------------------ 64x64 triangular inverses
 // Inverse of the unit-lower (L) or upper (U) 64x64 diagonal block at (r0, r0)
 // of every node, by substitution on the identity in shared memory. The

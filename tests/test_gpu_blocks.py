@@ -82,3 +82,24 @@ def test_laswp_forms_bitwise_equal():
         assert r.returncode == 0, r.stderr[-2000:]
         out[form] = r.stdout.strip().splitlines()[-1]
     assert out["warp"] == out["smem"]
+
+
+@pytest.mark.parametrize("n,lu", [(1000, 2), (1000, 4), (1500, 7), (2200, 16), (2048, 16)])
+def test_composed_block_interchanges_bitwise_equal(n, lu, monkeypatch):
+    """The outer block's np net permutations composed and applied in one pass
+    (launch_laswp_block, default) move the same rows as one pass per panel
+    (FEASTLAB_LASWP_BLOCK=0): the filtered block is bitwise identical, on
+    ragged last blocks and on blocks that end the matrix too."""
+    import paper_1605_08771_b200 as P
+    monkeypatch.setenv("FEASTLAB_LU_PANELS", str(lu))
+    A = O.random_symmetric(n, 41) / np.sqrt(n)
+    X = O.random_block(n, 72, 42)
+    rule = P.build_contour_rule(P.SearchInterval(-0.3, 0.2), 8)
+    out = {}
+    for form in ("0", "1"):
+        monkeypatch.setenv("FEASTLAB_LASWP_BLOCK", form)
+        out[form] = [P.apply_filter(A, rule, X) for _ in range(2)]  # eager, then graph
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][0])
+    ref = O.apply_filter(A, O.build_contour_rule(O.SearchInterval(-0.3, 0.2), 8), X)
+    assert np.linalg.norm(out["1"][0] - ref) / np.linalg.norm(ref) <= 1e-12
