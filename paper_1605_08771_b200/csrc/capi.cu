@@ -478,8 +478,10 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
                 // the block's earlier L columns must carry panel j-1's
                 // interchanges before they update panel j (the last panel's
                 // reach them on st, off the look-ahead chain)
-                if (j >= 2) swaps(tabs[j - 1], k0, kj - T, 0, 0, sp);
-                for (int i = 0; i < j; ++i) swaps(tabs[i], kj, kj + T, 0, 0, sp);
+                if (!f->laswp_block) {
+                    if (j >= 2) swaps(tabs[j - 1], k0, kj - T, 0, 0, sp);
+                    for (int i = 0; i < j; ++i) swaps(tabs[i], kj, kj + T, 0, 0, sp);
+                }
                 for (int i = 0; i < j; ++i) {
                     const int ki = k0 + i * T;
                     linv(ki, kj, T, sp);
@@ -488,6 +490,9 @@ void factor_group(fl_filter* f, int g0, int G, int s0, cudaStream_t st, cudaStre
                 sub(N - kj, T, j * T, kj, k0, k0, kj, kj, kj, sp, 2);
             }
             panel(kj, tabs[j]);
+            // one pass per panel over the block's other columns (the last
+            // panel's reach the columns left of it on st)
+            if (f->laswp_block && j + 1 < np) swaps(tabs[j], k0, kj, kj + T, c0, sp);
         }
         CK(cudaEventRecord(ev_panel, sp));
         CK(cudaStreamWaitEvent(st, ev_panel, 0));
