@@ -536,6 +536,11 @@ def run_b200(args, rank, world, local_rank):
                                         "form issues 6MNK on the DMMA pipe",
                      "tensor_pipe_frac": round(achieved * (0.75 if mode == "3m" else 1.0)
                                                / FP64_DMMA_PEAK_TFLOPS, 4),
+                     # the same issued work over the timed step itself (8 node
+                     # chunks in flight, everything else included)
+                     "tensor_pipe_frac_step": round(
+                         zflops / prof_steps * (0.75 if mode == "3m" else 1.0)
+                         / (ms / args.steps * 1e-3) / 1e12 / (FP64_DMMA_PEAK_TFLOPS * world), 4),
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": traffic,
