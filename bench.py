@@ -14,8 +14,9 @@ BASELINE.json names for the 1/2/4/8-GPU strong-scaling run; it fits one B200.
 
 Under torchrun (N > 1) each rank owns n_c/N contiguous nodes; timing is the
 max over ranks of CUDA-event time on the library stream. --impl reference
-times the CPU oracle (the reference's algorithm restated on OpenBLAS; the
-reference itself needs Eigen, which is absent) on the host cores.
+times the reference's CPU implementation on the host cores: its own sources
+compiled against oracle/eigen_shim (oracle/_ref, built where /root/reference
+exists; Eigen itself is absent), else the oracle restatement on OpenBLAS.
 """
 from __future__ import annotations
 
@@ -180,10 +181,15 @@ def build_workload(cfg_index, device):
     return A, vals, c
 
 
-def cpu_sample(c, threads, n=None, node=0):
-    """Oracle (restated reference algorithm) on one contour node of the workload:
+def cpu_sample(c, threads, n=None, node=0, backend="port"):
+    """The reference's CPU algorithm on one contour node of the workload:
     one zI - A LU + m0-RHS solve + accumulation = F_filter / n_c flops, at
-    order n (default: the workload's), node `node` of the workload's rule."""
+    order n (default: the workload's), node `node` of the workload's rule.
+    backend "port": the oracle restatement (oracle/liboracle.so); "reference":
+    the reference's own unmodified sources compiled against oracle/eigen_shim
+    (oracle/_ref/libfeastlab_ref.so, built where /root/reference exists)."""
+    import contextlib
+
     import oracle as O
 
     O.set_threads(threads)
@@ -196,9 +202,10 @@ def cpu_sample(c, threads, n=None, node=0):
     k = node % c["n_c"]
     one = O.ContourRule(rule.interval, rule.nodes[k:k + 1], rule.weights[k:k + 1])
     del M
-    t0 = time.perf_counter()
-    O.apply_filter(A, one, X)
-    dt = time.perf_counter() - t0
+    with (O.reference_backend() if backend == "reference" else contextlib.nullcontext()):
+        t0 = time.perf_counter()
+        O.apply_filter(A, one, X)
+        dt = time.perf_counter() - t0
     flops = filter_flops(n, p, 1)
     return flops / dt / 1e9, dt, n
 
@@ -232,9 +239,9 @@ def workload_config(args, c, world):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
-    """The reference's algorithm on the host cores (oracle/ = proj/src/filterop.cpp
-    restated on OpenBLAS; Eigen is absent, so the reference itself cannot be
-    built). Each timed step is one contour node of the workload (shift, LU,
+    """The reference's algorithm on the host cores: oracle/_ref (the reference's
+    unmodified proj/src/*.cpp against oracle/eigen_shim) when it was built, else
+    the oracle restatement of proj/src/filterop.cpp on OpenBLAS. Each timed step is one contour node of the workload (shift, LU,
     m0-RHS solve, accumulate: F_filter / n_c flops) at the workload's order
     when K such nodes fit REF_BUDGET_S, else at the largest multiple of 1024
     that does (said in `sample`); the line also extrapolates the whole
@@ -247,21 +254,28 @@ def run_reference(args, rank, world):
     vals = CF.spectrum(args.config, O.uniform_fill)
     c = CF.resolved(args.config, vals)
     threads = os.cpu_count() or 1
+    # the reference's own sources (oracle/_ref) where they were built, else the port
+    backend = "reference" if O.reference_available() else "port"
     # warm-up: thread pool and page faults, at a small order (untimed)
     for w in range(max(args.warmup, 0)):
-        cpu_sample(c, threads, n=min(c["n"], 2048), node=w)
+        cpu_sample(c, threads, n=min(c["n"], 2048), node=w, backend=backend)
     # rate probe (untimed) -> order of the timed samples
-    r0, _, _ = cpu_sample(c, threads, n=min(c["n"], 4096), node=0)
+    r0, _, _ = cpu_sample(c, threads, n=min(c["n"], 4096), node=0, backend=backend)
     per_step = REF_BUDGET_S / max(args.steps, 1)
     n_s = c["n"]
     while n_s > 1024 and filter_flops(n_s, c["m0"], 1) / (0.9 * r0 * 1e9) > per_step:
         n_s -= 1024
     rates, t_all = [], 0.0
     for k in range(args.steps):
-        r, dt, ns = cpu_sample(c, threads, n=n_s, node=k)
+        r, dt, ns = cpu_sample(c, threads, n=n_s, node=k, backend=backend)
         rates.append(r)
         t_all += dt
     value = float(np.mean(rates))
+    port = None
+    if backend == "reference":  # the restatement on the same sample, beside it (untimed)
+        rp, dtp, _ = cpu_sample(c, threads, n=n_s, node=0, backend="port")
+        port = {"value": round(rp, 3), "unit": "GFLOP/s", "seconds": round(dtp, 2),
+                "what": "oracle restatement (direct LAPACK calls) on node 0 of the same sample"}
     full = "the workload's order" if n_s == c["n"] else f"n={n_s} (workload n={c['n']}; " \
         f"{args.steps} steps x one node at full order would exceed the {REF_BUDGET_S:.0f} s budget)"
     line = {
@@ -271,11 +285,15 @@ def run_reference(args, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic",
         "config": workload_config(args, c, world),
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
-                         "kind": "port",
+                         "kind": backend,
                          "sample": f"one contour node per step (zI-A LU + m0={c['m0']} RHS solve + "
-                                   f"accumulate; node k of the rule at step k) at {full}; oracle "
-                                   "restatement of proj/src/filterop.cpp:9-84 on OpenBLAS "
-                                   "(reference needs Eigen, absent)",
+                                   f"accumulate; node k of the rule at step k) at {full}; " +
+                                   ("the reference's own proj/src/filterop.cpp compiled against "
+                                    "oracle/eigen_shim (Eigen API on OpenBLAS; Eigen itself is absent)"
+                                    if backend == "reference" else
+                                    "oracle restatement of proj/src/filterop.cpp:9-84 on OpenBLAS "
+                                    "(oracle/_ref was not built: no /root/reference at build time)"),
+                         "port": port,
                          "sample_n": n_s,
                          "extrapolated_s_per_application": round(
                              filter_flops(c["n"], c["m0"], c["n_c"]) / (value * 1e9), 1),
@@ -514,6 +532,14 @@ def run_b200(args, rank, world, local_rank):
                    # from the sampled rate (an n^3 LU dominates both)
                    "extrapolated_ms_per_step": round(filter_flops(n, p, nc) / (rate * 1e9) * 1e3,
                                                      1)}
+            import oracle as O
+            if O.reference_available():
+                rr_, dtr, nr = cpu_sample(c, threads, n=min(c["n"], CPU_SAMPLE_MAX_N),
+                                          backend="reference")
+                cpu["reference_build"] = {
+                    "value": round(rr_, 3), "unit": "GFLOP/s", "cores": threads,
+                    "sample": f"the same node (n={nr}) on oracle/_ref (the reference's own sources "
+                              f"+ oracle/eigen_shim) in {dtr:.2f} s"}
             # and on one core (a smaller node keeps it to a few seconds)
             r1, dt1, n1 = cpu_sample(c, 1, n=min(c["n"], 2048))
             cpu["one_core"] = {"value": round(r1, 3), "unit": "GFLOP/s", "cores": 1,
